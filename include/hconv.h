@@ -1,0 +1,132 @@
+/*
+ * hconv.h — C ABI of the hybrid-dealiased convolution path (arXiv 2303.17510).
+ *
+ * This is the drop-in boundary.  Two shared libraries export exactly these
+ * symbols:
+ *   paper_2303_17510_b200/_lib/libhconv_cuda.so  — the product: sm_100a kernels,
+ *        device pointers, asynchronous on a caller-supplied cudaStream_t.
+ *   oracle/_build/libhconv_oracle.so             — test infrastructure: the CPU
+ *        restatement of the reference, host pointers, synchronous.
+ * No C++ types, no exceptions and no torch types cross this boundary.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference):
+ *   hconv_derive_params      proj/include/hconv/plan.hpp:67   deriveParams
+ *   hconv_block_length       proj/src/plan.cpp:26-29          PlanParams::blockLength
+ *   hconv_stored_length      proj/src/plan.cpp:31-33          PlanParams::storedLength
+ *   hconv_padded_length      proj/include/hconv/plan.hpp:56   PlanParams::paddedLength
+ *   hconv_root               proj/include/hconv/plan.hpp:70   root
+ *   hconv_work_memory_words  proj/include/hconv/plan.hpp:79   workMemoryWords
+ *   hconv_root_table         proj/include/hconv/plan.hpp:84   RootTable
+ *   hconv_symmetry_name      proj/include/hconv/plan.hpp:27   name(Symmetry)
+ *   hconv_symmetry_from_name proj/include/hconv/plan.hpp:28   symmetryFromName
+ *   hconv_pfft_forward       SPEC.md:158,176,194,258,276,331,349  forward1/2/Inner[C|H]
+ *   hconv_pfft_backward      SPEC.md:167,185,203,267,285,340,358  backward1/2/Inner[C|H]
+ *   hconv_plan_create        SPEC.md:400-403 Conv1dPlan, SPEC.md:469-472 ConvPlanND,
+ *                            SPEC.md:533-550 tune_1d/tune_nd (when an axis has m == 0)
+ *   hconv_convolve           SPEC.md:406-423 convolve/convolveC/convolveH,
+ *                            SPEC.md:475-483 convolve_nd
+ * Exceptions of the reference (std::invalid_argument, plan.cpp:36-38,67,77-80,92-93)
+ * become HCONV_INVALID_ARG; the message is available from hconv_last_error().
+ */
+#ifndef HCONV_H
+#define HCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum hconv_status {
+  HCONV_OK = 0,
+  HCONV_INVALID_ARG = 1, /* L == 0, m == 0, M < L, arity, layout */
+  HCONV_UNSUPPORTED = 2, /* e.g. a block size no kernel instantiation covers */
+  HCONV_CUDA_ERROR = 3,
+  HCONV_NCCL_ERROR = 4,
+  HCONV_ALLOC = 5,
+  HCONV_INTERNAL = 6
+} hconv_status;
+
+/* plan.hpp:17 enum class Symmetry { Complex, Centered, Hermitian } */
+typedef enum hconv_symmetry { HCONV_COMPLEX = 0, HCONV_CENTERED = 1, HCONV_HERMITIAN = 2 } hconv_symmetry;
+/* plan.hpp:20 enum class Regime { P1, P2, Inner } */
+typedef enum hconv_regime { HCONV_P1 = 0, HCONV_P2 = 1, HCONV_INNER = 2 } hconv_regime;
+/* SPEC.md:424 builtin_mult_product: B = 1, elementwise product of the A inputs */
+typedef enum hconv_mult { HCONV_MULT_PRODUCT = 0 } hconv_mult;
+
+/* plan.hpp:39-62 PlanParams (field for field; kind = {symmetry, regime}) */
+typedef struct hconv_params {
+  size_t L, M, m, p, q, n, D, C, S;
+  int inplace;
+  int symmetry; /* hconv_symmetry */
+  int regime;   /* hconv_regime  */
+} hconv_params;
+
+/* ---- plan module (the reference's only compiled code) ---- */
+hconv_status hconv_derive_params(size_t L, size_t M, size_t m, int symmetry, hconv_params* out);
+size_t hconv_block_length(const hconv_params* pp);
+size_t hconv_stored_length(const hconv_params* pp);
+size_t hconv_padded_length(const hconv_params* pp);
+hconv_status hconv_root(size_t N, int64_t k, double* re, double* im);
+hconv_status hconv_work_memory_words(const hconv_params* pp, size_t A, size_t B, size_t d, size_t L,
+                                     uint64_t* implicit_words, double* explicit_words);
+/* Fills out[2k], out[2k+1] = Re, Im zeta_N^k for k in [0, N) (host memory in both libraries). */
+hconv_status hconv_root_table(size_t N, double* out);
+const char* hconv_symmetry_name(int symmetry);
+hconv_status hconv_symmetry_from_name(const char* name, int* symmetry);
+
+/* ---- residue-level padded FFTs (SPEC pfft-complex / pfft-centered / pfft-hermitian) ----
+ * Batched over pp->C copies: element j of copy c is at f[c*dist + j*pp->S] (complex128,
+ * interleaved re/im).  Forward writes, for each copy, the residue (block) contribution in
+ * the reference's order into F[c*blockLength ...]: complex kinds complex128
+ * F[u*m + l] = F_{q l + u n + r} (u = 0 for p <= 2), Hermitian kind float64 (real) values.
+ * Backward is the unnormalised inverse of one residue; with accumulate != 0 it adds into h.
+ * Hermitian data stores the non-negative logical indices 0..ceil(L/2)-1.
+ * Centered data stores logical index j - floor(L/2) at j.                               */
+hconv_status hconv_pfft_forward(const hconv_params* pp, const void* f, size_t dist, size_t residue, void* F,
+                                void* stream);
+hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t residue, void* h, size_t dist,
+                                 int accumulate, void* stream);
+
+/* ---- convolution plans ---- */
+typedef struct hconv_axis {
+  size_t L;     /* logical data length along the axis */
+  size_t M;     /* minimum dealiased length, M >= L */
+  size_t m;     /* subtransform size; 0 = let the device-timed planner choose */
+  int symmetry; /* hconv_symmetry */
+} hconv_axis;
+
+typedef struct hconv_desc {
+  int dims;              /* 1, 2 or 3; axis[dims-1] is the innermost (contiguous) axis */
+  hconv_axis axis[3];
+  size_t A, B;           /* inputs / outputs of the multiplication operator */
+  int mult;              /* hconv_mult */
+  size_t C;              /* 1D: number of independent copies (batch) */
+  size_t dist;           /* 1D: elements between copies; 0 = stored length */
+  int device;            /* CUDA ordinal (ignored by the oracle) */
+  int flags;             /* reserved, 0 */
+} hconv_desc;
+
+typedef struct hconv_plan hconv_plan;
+
+hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** plan);
+hconv_status hconv_plan_params(const hconv_plan* plan, int axis, hconv_params* out);
+/* Bytes of device scratch the plan owns (0 for the oracle). */
+size_t hconv_plan_workspace_bytes(const hconv_plan* plan);
+/* in[A], out[B]: complex128 arrays with the stored layout of the descriptor.
+ * out[b] == in[b] (in place, the reference's convention, Alg. convolve) is allowed.
+ * CUDA library: device pointers, asynchronous on stream (cudaStream_t, NULL = legacy).
+ * Oracle: host pointers, stream ignored.                                           */
+hconv_status hconv_convolve(hconv_plan* plan, const void* const* in, void* const* out, void* stream);
+hconv_status hconv_plan_destroy(hconv_plan* plan);
+const char* hconv_last_error(void);
+/* Library identity: "cuda-sm_100a" or "oracle-cpu". */
+const char* hconv_backend(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HCONV_H */
