@@ -1,0 +1,23 @@
+/*
+ * hconv_ext.h — utilities exported by libhconv_cuda.so that are NOT part of the reference's
+ * API (bench / test support).  The oracle library does not export these.
+ */
+#ifndef HCONV_EXT_H
+#define HCONV_EXT_H
+#include "hconv.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+/* Counter-based synthetic inputs on the device: element i gets
+ * Re, Im = 2u-1, u = (splitmix64(seed*phi + (a<<56 | comp<<55 | (first_index+i))) >> 11) 2^-53. */
+hconv_status hconv_util_fill_uniform(uint64_t seed, uint64_t a, uint64_t first_index, size_t count, void* out,
+                                     void* stream);
+/* Planner report of the last tuning done for this plan: rows (m, p, q, n, block, median ms);
+ * returns the row count, or -(count+1) when the choice came from the planner cache. */
+int hconv_plan_report(const hconv_plan* plan, double* out, int cap);
+/* Radix plan of the kernel serving an axis ("16x16x24", "direct", ...). */
+const char* hconv_plan_kernel(const hconv_plan* plan, int axis);
+#ifdef __cplusplus
+}
+#endif
+#endif

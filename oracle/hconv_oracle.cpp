@@ -887,9 +887,9 @@ int oracle_forward_conjugate_pair(const hconv_params* pp, const double* f, size_
 }
 int oracle_direct_convolution(int dims, const int* syms, const size_t* Ls, const double* f, const double* g, double* out) {
   try {
-    double macs = 1;
-    for (int k = 0; k < dims; ++k) macs *= (double)Ls[k] * (double)Ls[k] * 4.0;
-    if (macs > 1e9) throw std::invalid_argument("direct_convolution: guard exceeded (SPEC.md:588)");
+    double macs = 1;  // stored outputs x full logical input points
+    for (int k = 0; k < dims; ++k) macs *= (double)Ls[k] * (double)Ls[k];
+    if (macs > 2e9) throw std::invalid_argument("direct_convolution: guard exceeded (SPEC.md:588)");
     direct_conv(dims, syms, Ls, (const cd*)f, (const cd*)g, (cd*)out);
   } catch (const std::exception& e) { g_err = e.what(); return 1; }
   return 0;

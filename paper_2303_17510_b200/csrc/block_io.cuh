@@ -1,0 +1,148 @@
+// block_io.cuh — per-symmetry residue-block pre/post-processing shared by every kernel.
+//
+// Unified form of the paper's padded FFTs.  For an axis with parameters (L, M, m, p, q, n)
+// let B be the residue-block length (blockLength(), proj/src/plan.cpp:26-29) so that
+// q m = n B in every regime.  Residue block v of the qm-point padded transform is
+//     F_{v + n k} = sum_s zeta_B^{k s} W_s,   W_s = sum_{j == s (mod B)} zeta_qm^{v j} f_j,
+// the B-point DFT of the pre-twiddled input folded modulo B:
+//   * complex, p <= 2 : Alg. forward1/forward2, W_s = w_{r,s};
+//   * complex, p > 2  : Alg. forwardInner -- the p-point DFTs over t are
+//                       the first radix-p stage of the pm-point DFT, k = p l + u;
+//   * centered        : Eqs. forCent/wDef, logical j in [-H, L-H);
+//   * Hermitian       : Eq. wHerDef; W is Hermitian so the B-point DFT is
+//                       real and is computed as a complex-to-real transform through one
+//                       B/2-point complex FFT (Z'_k packing below).
+// The inverse of residue v is h_j += zeta_qm^{-v j} w_{j mod B}, w = unnormalised inverse
+// B-point DFT of the product (Eqs. invStan/invInner).
+#pragma once
+#include "fft_device.cuh"
+
+namespace hc {
+
+enum : int { SYM_COMPLEX = 0, SYM_CENTERED = 1, SYM_HERMITIAN = 2 };
+
+// Line addressing: line l starts at (l / nin) * d_out + (l % nin) * d_in (complex elements);
+// element j of the line is at start + j * es.
+struct Lines {
+  long long count, nin, d_out, d_in, es;
+  __device__ __forceinline__ long long base(long long l) const { return (l / nin) * d_out + (l % nin) * d_in; }
+};
+
+struct AxisDev {
+  int sym;
+  int L;   // logical length
+  int S;   // stored length (L, or ceil(L/2) for Hermitian)
+  int B;   // residue block length
+  int Bc;  // complex FFT length (B, or B/2 for Hermitian)
+  int n;   // residue blocks
+  int qm;  // padded length q*m = n*B
+  int H;   // centered origin floor(L/2)
+  int pe;  // reference-order interleave: p (complex inner), p/2 (centered/Hermitian inner), else 1
+  int m;
+  const double2* tw;  // zeta_Bc^e, e < Bc
+  const double2* zq;  // zeta_qm^e, e < qm
+};
+
+// zeta_qm^e for |e| < 2^31 (32-bit reduction: exponents are v*j with v < n, |j| < 2B)
+__device__ __forceinline__ double2 zpow(const AxisDev& a, int e) {
+  e %= a.qm;
+  if (e < 0) e += a.qm;
+  return __ldg(a.zq + e);
+}
+
+// W_s for complex / centered data (s in [0, B)).
+template <int SYM>
+__device__ __forceinline__ double2 load_W(const AxisDev& a, const double2* __restrict__ f, long long es, int s, int v) {
+  double2 acc = make_double2(0.0, 0.0);
+  if constexpr (SYM == SYM_COMPLEX) {
+    for (int j = s; j < a.L; j += a.B) acc = cadd(acc, v ? cmul(f[(long long)j * es], zpow(a, v * j)) : f[(long long)j * es]);
+  } else {
+    // logical j = s (stored s + H) and j = s - B (stored s - B + H)
+    if (s < a.L - a.H) acc = v ? cmul(f[(long long)(s + a.H) * es], zpow(a, v * s)) : f[(long long)(s + a.H) * es];
+    const int st2 = s - a.B + a.H;
+    if (st2 >= 0) {
+      const double2 x = f[(long long)st2 * es];
+      acc = cadd(acc, v ? cmul(x, zpow(a, v * (s - a.B))) : x);
+    }
+  }
+  return acc;
+}
+
+// Hermitian W_s, s in [0, B/2]: logical j = s (f_s) and j = s - B (conj f_{B-s}).
+__device__ __forceinline__ double2 load_WH(const AxisDev& a, const double2* __restrict__ f, long long es, int s, int v) {
+  double2 acc = make_double2(0.0, 0.0);
+  if (s < a.S) acc = v ? cmul(f[(long long)s * es], zpow(a, v * s)) : f[(long long)s * es];
+  const int r = a.B - s;
+  if (r > 0 && r < a.S) {
+    const double2 x = cconj(f[(long long)r * es]);
+    acc = cadd(acc, v ? cmul(x, zpow(a, v * (s - a.B))) : x);
+  }
+  return acc;
+}
+
+// Packed complex-to-real input: Z'_k = (W_k + conj W_{Bc-k}) + i zeta_B^k (W_k - conj W_{Bc-k}),
+// so that the Bc-point forward DFT of Z' is z_l = V_{2l} + i V_{2l+1}.
+__device__ __forceinline__ double2 load_Zp(const AxisDev& a, const double2* __restrict__ f, long long es, int k, int v) {
+  const double2 wk = load_WH(a, f, es, k, v);
+  const double2 wm = cconj(load_WH(a, f, es, a.Bc - k, v));
+  const double2 e = cadd(wk, wm);
+  const double2 o = cmul(csub(wk, wm), __ldg(a.zq + (long long)k * a.n));  // zeta_B^k = zeta_qm^{k n}
+  return make_double2(e.x - o.y, e.y + o.x);                                 // e + i o
+}
+
+// value of block index s in pass-0 order for the given symmetry
+template <int SYM>
+__device__ __forceinline__ double2 load_in(const AxisDev& a, const double2* __restrict__ f, long long es, int s, int v) {
+  if constexpr (SYM == SYM_HERMITIAN) return load_Zp(a, f, es, s, v);
+  else return load_W<SYM>(a, f, es, s, v);
+}
+
+// Destination of residue contributions: dst[j] = ((acc ? acc[j] : 0) + val) * scale.
+struct Emit {
+  double2* dst;
+  long long des;
+  const double2* acc;
+  long long aes;
+  double scale;
+  __device__ __forceinline__ void operator()(long long j, double2 val) const {
+    if (acc) val = cadd(val, acc[j * aes]);
+    if (scale != 1.0) val = cscale(val, scale);
+    dst[j * des] = val;
+  }
+};
+
+// Complex / centered inverse post-processing of block element s (natural order).
+template <int SYM>
+__device__ __forceinline__ void store_w(const AxisDev& a, const Emit& em, int s, int v, double2 w) {
+  if constexpr (SYM == SYM_COMPLEX) {
+    for (int j = s; j < a.L; j += a.B) em(j, v ? cmulc(w, zpow(a, v * j)) : w);
+  } else {
+    if (s < a.L - a.H) em(s + a.H, v ? cmulc(w, zpow(a, v * s)) : w);
+    const int st2 = s - a.B + a.H;
+    if (st2 >= 0) em(st2, v ? cmulc(w, zpow(a, v * (s - a.B))) : w);
+  }
+}
+
+// Hermitian inverse post-processing: Z (natural order, Bc values, shared memory) holds the
+// Bc-point inverse DFT of the packed product; output stored index j in [0, S).
+__device__ __forceinline__ double2 herm_w(const AxisDev& a, const double2* Z, int j, int v) {
+  const bool hi = j > a.Bc;
+  const int k = hi ? a.B - j : j;
+  const double2 zk = Z[k == a.Bc ? 0 : k];
+  const double2 zm = cconj(Z[k == 0 ? 0 : a.Bc - k]);
+  const double2 e = cscale(cadd(zk, zm), 0.5);
+  const double2 d = cscale(csub(zk, zm), 0.5);
+  const double2 o = make_double2(d.y, -d.x);                              // d / i
+  double2 w = cadd(e, cmulc(o, __ldg(a.zq + (long long)k * a.n)));         // e + zeta_B^{-k} o
+  if (hi) w = cconj(w);
+  return v ? cmulc(w, zpow(a, v * j)) : w;
+}
+
+// reference order of block value with natural index k' (SPEC pfft-* output: F[u m + l] with
+// k' = pe*l + u for inner regimes, F[l] otherwise)
+__device__ __forceinline__ long long ref_index(const AxisDev& a, long long kp) {
+  if (a.pe <= 1) return kp;
+  return (kp % a.pe) * a.m + kp / a.pe;
+}
+
+}  // namespace hc

@@ -1,0 +1,307 @@
+// fft_device.cuh — in-register / shared-memory FP64 complex FFT building blocks (sm_100a).
+//
+// Sign convention of the paper: the forward transform uses
+// zeta_N = exp(+2 pi i / N) (DIR = +1); the unnormalised inverse uses DIR = -1.
+//
+// A block FFT of compile-time length N = R_0 R_1 ... R_{P-1} runs as P passes.  Pass i
+// takes the sub-sequences left by passes 0..i-1 (indexed by K = k_0 + R_0 k_1 + ..., each of
+// length Ns_i = R_i ... R_{P-1}), does an R_i-point DFT in registers over the elements
+// (K, Ns_{i+1} a + b), a < R_i, multiplies output k by omega_{Ns_i}^{b k} and hands
+// element (K + Rprod_i k, b) to pass i+1 through one shared-memory exchange.  Input is in
+// natural order, output index K = k_0 + R_0 k_1 + ... is the natural frequency.  Because a
+// convolution only needs F and G in the SAME order, the forward leaves its last pass in
+// registers, the pointwise product is taken there, and the inverse runs the passes in
+// reverse from the same registers (no bit-reversal, no extra round trip).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "tw_consts.h"
+
+namespace hc {
+
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    sfor<N, I + 1>(static_cast<F&&>(f));
+  }
+}
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// a * i^DIR
+template <int DIR>
+__device__ __forceinline__ double2 mul_i(double2 a) {
+  if constexpr (DIR > 0) return make_double2(-a.y, a.x);
+  else return make_double2(a.y, -a.x);
+}
+// multiply by a table twiddle (DIR = +1) or its conjugate (DIR = -1)
+template <int DIR>
+__device__ __forceinline__ double2 mul_tw(double2 a, double2 w) {
+  if constexpr (DIR > 0) return cmul(a, w);
+  else return cmulc(a, w);
+}
+
+// x * zeta_R^{DIR*E}, trivial angles folded at compile time.
+template <int R, int E, int DIR>
+__device__ __forceinline__ double2 twc(double2 x) {
+  constexpr int e = ((E % R) + R) % R;
+  if constexpr (e == 0) {
+    return x;
+  } else if constexpr (2 * e == R) {
+    return make_double2(-x.x, -x.y);
+  } else if constexpr (4 * e == R) {
+    return mul_i<DIR>(x);
+  } else if constexpr (4 * e == 3 * R) {
+    return mul_i<-DIR>(x);
+  } else {
+    constexpr double c = TwC<R>::c[e];
+    constexpr double s = DIR * TwC<R>::s[e];
+    return make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c));
+  }
+}
+
+constexpr int first_factor(int R) {
+  if (R % 4 == 0 && R != 4) return 4;
+  for (int f : {2, 3, 5, 7}) if (R % f == 0 && R != f) return f;
+  return R;  // prime
+}
+
+// In-place R-point DFT of x[0..R) in registers, natural-order output.
+template <int R, int DIR>
+struct DFT {
+  static __device__ __forceinline__ void run(double2* x) {
+    constexpr int A = first_factor(R);
+    if constexpr (A == R) {  // prime: direct sum with compile-time twiddles
+      double2 y[R];
+      sfor<R>([&](auto K) {
+        constexpr int k = K;
+        double2 acc = x[0];
+        sfor<R - 1>([&](auto J) {
+          constexpr int j = J + 1;
+          acc = cadd(acc, twc<R, j * k, DIR>(x[j]));
+        });
+        y[k] = acc;
+      });
+      sfor<R>([&](auto K) { x[K] = y[K]; });
+    } else {  // four-step: n = Bf a + b, k = ka + A kb
+      constexpr int Bf = R / A;
+      double2 t[R];
+      sfor<Bf>([&](auto Bi) {
+        constexpr int b = Bi;
+        double2 y[A];
+        sfor<A>([&](auto Ai) { y[Ai] = x[Bf * Ai + b]; });
+        DFT<A, DIR>::run(y);
+        sfor<A>([&](auto Ki) {
+          constexpr int ka = Ki;
+          t[ka * Bf + b] = twc<R, b * ka, DIR>(y[ka]);
+        });
+      });
+      sfor<A>([&](auto Ki) {
+        constexpr int ka = Ki;
+        double2 z[Bf];
+        sfor<Bf>([&](auto Bi) { z[Bi] = t[ka * Bf + Bi]; });
+        DFT<Bf, DIR>::run(z);
+        sfor<Bf>([&](auto Kb) { x[ka + A * Kb] = z[Kb]; });
+      });
+    }
+  }
+};
+template <int DIR>
+struct DFT<1, DIR> {
+  static __device__ __forceinline__ void run(double2*) {}
+};
+template <int DIR>
+struct DFT<2, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  }
+};
+template <int DIR>
+struct DFT<3, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    constexpr double s3 = DIR * 0.8660254037844386;  // sin(2 pi / 3)
+    const double2 t1 = cadd(x[1], x[2]);
+    const double2 t2 = make_double2(fma(-0.5, t1.x, x[0].x), fma(-0.5, t1.y, x[0].y));
+    const double2 d = csub(x[1], x[2]);
+    const double2 t3 = make_double2(-s3 * d.y, s3 * d.x);  // i * s3 * d
+    x[0] = cadd(x[0], t1);
+    x[1] = cadd(t2, t3);
+    x[2] = csub(t2, t3);
+  }
+};
+template <int DIR>
+struct DFT<4, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    const double2 t0 = cadd(x[0], x[2]), t1 = csub(x[0], x[2]);
+    const double2 t2 = cadd(x[1], x[3]), t3 = mul_i<DIR>(csub(x[1], x[3]));
+    x[0] = cadd(t0, t2);
+    x[2] = csub(t0, t2);
+    x[1] = cadd(t1, t3);
+    x[3] = csub(t1, t3);
+  }
+};
+
+// ---------------------------------------------------------------- block FFT --
+template <int... Rs>
+struct Radices {
+  static constexpr int P = sizeof...(Rs);
+  static constexpr int R[P] = {Rs...};
+  static constexpr int N = (Rs * ... * 1);
+};
+
+template <class RL, int T_>
+struct FFTCfg {
+  static constexpr int N = RL::N;
+  static constexpr int P = RL::P;
+  static constexpr int T = T_;
+  static constexpr int R(int i) { return RL::R[i]; }
+  static constexpr int Ns(int i) {  // sub-sequence length before pass i (Ns(P) = 1)
+    int v = 1;
+    for (int k = i; k < P; ++k) v *= RL::R[k];
+    return v;
+  }
+  static constexpr int Rprod(int i) {
+    int v = 1;
+    for (int k = 0; k < i; ++k) v *= RL::R[k];
+    return v;
+  }
+  static constexpr int NB(int i) { return N / RL::R[i]; }                // butterflies in pass i
+  static constexpr int C(int i) { return (NB(i) + T - 1) / T; }          // butterflies per thread
+  static constexpr int E_calc() {
+    int e = 0;
+    for (int i = 0; i < P; ++i) e = (C(i) * RL::R[i] > e) ? C(i) * RL::R[i] : e;
+    return e;
+  }
+  static constexpr int E = E_calc();                                     // registers (complex) per thread
+  static constexpr int St(int i) { return Ns(i) + ((Ns(i) % 2 == 0) ? 1 : 0); }  // padded row (odd)
+  static constexpr int X_calc() {
+    int x = N;
+    for (int i = 1; i < P; ++i) x = (Rprod(i) * St(i) > x) ? Rprod(i) * St(i) : x;
+    return x;
+  }
+  static constexpr int XS = X_calc();                                    // exchange buffer (complex)
+  static constexpr int ES = C(P - 1) * RL::R[P - 1];                     // last-pass values per thread
+};
+
+// Group barrier over NT threads (named barrier id; NT must be a multiple of 32).
+struct GroupSync {
+  int id, nt;
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+  }
+};
+
+// Forward FFT: v holds pass-0 inputs (v[c*R0 + a] = x[Ns1*a + b], b = tid + c*T).
+// On return v holds the last pass outputs: v[c*R + k] = X[beta + Rprod(P-1)*k], beta = tid + c*T.
+// tw: zeta_N^e (e < N) in global memory.
+template <class Cfg, int DIR, class Sync>
+__device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* __restrict__ tw,
+                                            int tid, const Sync& sync) {
+  constexpr int P = Cfg::P, T = Cfg::T;
+  sfor<P>([&](auto I) {
+    constexpr int i = I;
+    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
+    sfor<C>([&](auto Ci) {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (NB % T == 0 || beta < NB) {
+        DFT<R, DIR>::run(v + c * R);
+        if constexpr (i < P - 1) {
+          const int b = beta % Ns1;
+          sfor<R - 1>([&](auto Ki) {
+            constexpr int k = Ki + 1;
+            v[c * R + k] = mul_tw<DIR>(v[c * R + k], __ldg(tw + b * k * Rp));
+          });
+        }
+      }
+    });
+    if constexpr (i < P - 1) {
+      constexpr int St = Cfg::St(i + 1);
+      sfor<C>([&](auto Ci) {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB % T == 0 || beta < NB) {
+          const int K = beta / Ns1, b = beta % Ns1;
+          sfor<R>([&](auto Ki) { X[(K + Rp * Ki) * St + b] = v[c * R + Ki]; });
+        }
+      });
+      sync();
+      constexpr int R2 = Cfg::R(i + 1), C2 = Cfg::C(i + 1), NB2 = Cfg::NB(i + 1), Ns2 = Cfg::Ns(i + 2);
+      sfor<C2>([&](auto Ci) {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB2 % T == 0 || beta < NB2) {
+          const int K = beta / Ns2, b = beta % Ns2;
+          sfor<R2>([&](auto Ai) { v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b]; });
+        }
+      });
+      sync();
+    }
+  });
+}
+
+// Inverse FFT (DIR = -1 of the forward), starting from the last-pass layout left by
+// fft_forward and ending in the pass-0 layout (v[c*R0 + a] = x[Ns1*a + b]).
+template <class Cfg, class Sync>
+__device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* __restrict__ tw,
+                                            int tid, const Sync& sync) {
+  constexpr int P = Cfg::P, T = Cfg::T;
+  sfor<P>([&](auto Iv) {
+    constexpr int i = P - 1 - Iv;
+    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
+    sfor<C>([&](auto Ci) {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (NB % T == 0 || beta < NB) {
+        if constexpr (i < P - 1) {
+          const int b = beta % Ns1;
+          sfor<R - 1>([&](auto Ki) {
+            constexpr int k = Ki + 1;
+            v[c * R + k] = cmulc(v[c * R + k], __ldg(tw + b * k * Rp));
+          });
+        }
+        DFT<R, -1>::run(v + c * R);
+      }
+    });
+    if constexpr (i > 0) {
+      constexpr int St = Cfg::St(i);
+      sfor<C>([&](auto Ci) {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB % T == 0 || beta < NB) {
+          const int K = beta / Ns1, b = beta % Ns1;
+          sfor<R>([&](auto Ai) { X[K * St + Ns1 * Ai + b] = v[c * R + Ai]; });
+        }
+      });
+      sync();
+      constexpr int R0 = Cfg::R(i - 1), C0 = Cfg::C(i - 1), NB0 = Cfg::NB(i - 1), Rp0 = Cfg::Rprod(i - 1);
+      constexpr int Ns0 = Cfg::Ns(i);  // row length of the exchange
+      sfor<C0>([&](auto Ci) {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB0 % T == 0 || beta < NB0) {
+          const int K = beta / Ns0, b = beta % Ns0;
+          sfor<R0>([&](auto Ki) { v[c * R0 + Ki] = X[(K + Rp0 * Ki) * St + b]; });
+        }
+      });
+      sync();
+    }
+  });
+}
+
+}  // namespace hc

@@ -1,0 +1,747 @@
+// hconv_lib.cu — host side of libhconv_cuda.so: the C ABI of include/hconv.h, plan objects,
+// kernel selection, the device-timed m/p/q planner and the N-D decomposition driver.
+//
+// Reference interfaces (paths relative to /root/reference):
+//   plan module          proj/include/hconv/plan.hpp:10-108, proj/src/plan.cpp:1-101
+//   Conv1dPlan/convolve  SPEC.md:400-423, Algs. convolve/convolveX PAPER.md:188-262
+//   ConvPlanND
+//   tune_1d / tune_nd    SPEC.md:518-572, PAPER.md:894-914 (device events replace the CPU clock)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/hconv.h"
+#include "../../include/hconv_ext.h"
+#include "plan.hpp"
+#include "registry.cuh"
+
+namespace hc {
+void registry_sym0(KernelEntry* out, int* count);
+void registry_sym1(KernelEntry* out, int* count);
+void registry_sym2(KernelEntry* out, int* count);
+}  // namespace hc
+
+using hc::KernelEntry;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct Unsupported : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CK(x)                                                                                 \
+  do {                                                                                        \
+    cudaError_t e_ = (x);                                                                     \
+    if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+template <class F>
+hconv_status guarded(F&& f) {
+  try {
+    f();
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return HCONV_INVALID_ARG;
+  } catch (const Unsupported& e) {
+    g_err = e.what();
+    return HCONV_UNSUPPORTED;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return HCONV_CUDA_ERROR;
+  } catch (const std::bad_alloc& e) {
+    g_err = "host allocation failed";
+    return HCONV_ALLOC;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return HCONV_INTERNAL;
+  }
+  return HCONV_OK;
+}
+
+// ------------------------------------------------------------ registry ------
+struct Registry {
+  KernelEntry e[3][32];
+  int n[3] = {0, 0, 0};
+  Registry() {
+    hc::registry_sym0(e[0], &n[0]);
+    hc::registry_sym1(e[1], &n[1]);
+    hc::registry_sym2(e[2], &n[2]);
+  }
+};
+const Registry& registry() {
+  static Registry r;
+  return r;
+}
+
+// kernel for (symmetry, complex FFT length); naive entry for small non-radix lengths
+const KernelEntry* find_kernel(int sym, int Bc, bool allow_naive = true) {
+  const Registry& r = registry();
+  const KernelEntry* naive = nullptr;
+  for (int i = 0; i < r.n[sym]; ++i) {
+    if (r.e[sym][i].naive) naive = &r.e[sym][i];
+    else if (r.e[sym][i].Bc == Bc) return &r.e[sym][i];
+  }
+  if (allow_naive && naive && Bc <= hc::kNaiveMax) return naive;
+  return nullptr;
+}
+
+struct DevInfo {
+  int sms = 0;
+  std::string name;
+};
+DevInfo dev_info() {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  static std::mutex mu;
+  static std::map<int, DevInfo> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(d);
+  if (it != cache.end()) return it->second;
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, d));
+  DevInfo di{prop.multiProcessorCount, prop.name};
+  cache[d] = di;
+  return di;
+}
+
+// one-time per (function, device) attribute setting and occupancy query
+int occupancy(const void* fn, int threads, size_t smem) {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, int, size_t>, int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_tuple(fn, d, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  // the attribute is per function: only ever raise it (launches with less smem stay valid)
+  static std::map<std::pair<const void*, int>, size_t> attr;
+  size_t& cur = attr[std::make_pair(fn, d)];
+  if (smem > cur) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cur = smem;
+  }
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+  if (nb < 1) throw Unsupported("kernel does not fit on an SM");
+  cache[key] = nb;
+  return nb;
+}
+
+// ------------------------------------------------------- device tables ------
+struct DevTable {
+  double2* ptr = nullptr;
+};
+// zeta_N^e, e < N, computed on the host with exact integer reduction (plan.cpp:66-73,91-99)
+const double2* root_table(size_t N) {
+  int d = 0;
+  CK(cudaGetDevice(&d));
+  static std::mutex mu;
+  static std::map<std::pair<int, size_t>, DevTable> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair(d, N);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.ptr;
+  std::vector<double2> h(N);
+  for (size_t k = 0; k < N; ++k) {
+    const hb::Complex z = hb::root(N, (int64_t)k);
+    h[k] = make_double2(z.real(), z.imag());
+  }
+  DevTable t;
+  CK(cudaMalloc(&t.ptr, N * sizeof(double2)));
+  CK(cudaMemcpy(t.ptr, h.data(), N * sizeof(double2), cudaMemcpyHostToDevice));
+  cache[key] = t;
+  return t.ptr;
+}
+
+// ----------------------------------------------------------- axis plans -----
+struct AxisPlan {
+  hb::PlanParams pp;
+  hc::AxisDev dev{};
+  const KernelEntry* k = nullptr;
+  size_t data = 0;  // values per line (dataLength)
+};
+
+hb::Symmetry to_sym(int s) {
+  if (s < 0 || s > 2) throw std::invalid_argument("bad symmetry");
+  return static_cast<hb::Symmetry>(s);
+}
+
+int complex_len(const hb::PlanParams& pp) {
+  const size_t B = pp.blockLength();
+  if (pp.symmetry == hb::Symmetry::Hermitian && B % 2 == 0) return (int)(B / 2);
+  return (int)B;
+}
+
+// Build the device view of one axis; throws Unsupported if no kernel covers the block.
+AxisPlan make_axis(const hb::PlanParams& pp, bool allow_naive = true) {
+  AxisPlan ap;
+  ap.pp = pp;
+  ap.data = pp.dataLength();
+  const size_t B = pp.blockLength(), qm = pp.paddedLength();
+  if (qm != pp.n * B) throw std::logic_error("qm != n B");
+  if (qm > (size_t)INT32_MAX / 4) throw Unsupported("padded length too large");
+  const int sym = (int)pp.symmetry;
+  const int Bc = complex_len(pp);
+  ap.k = find_kernel(sym, Bc, allow_naive);
+  if (!ap.k) throw Unsupported("no kernel for block length " + std::to_string(B) + " (" + hb::name(pp.symmetry) + ")");
+  hc::AxisDev& a = ap.dev;
+  a.sym = sym;
+  a.L = (int)pp.L;
+  a.S = (int)pp.dataLength();
+  a.B = (int)B;
+  a.Bc = Bc;
+  a.n = (int)pp.n;
+  a.qm = (int)qm;
+  a.H = (int)(pp.L / 2);
+  a.pe = (int)pp.interleave();
+  a.m = (int)pp.m;
+  a.tw = root_table((size_t)Bc);
+  a.zq = root_table(qm);
+  return ap;
+}
+
+size_t smem_conv(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_conv * ap.dev.Bc : ap.k->smem_conv; }
+size_t smem_fwd(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_fwd * ap.dev.Bc : ap.k->smem_fwd; }
+size_t smem_bwd(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_bwd * ap.dev.Bc : ap.k->smem_bwd; }
+
+int grid_for(const void* fn, const KernelEntry* k, size_t smem, long long items) {
+  const int nb = occupancy(fn, k->T * k->G, smem);
+  const long long need = (items + k->G - 1) / k->G;
+  const long long cap = (long long)nb * dev_info().sms;
+  return (int)std::max<long long>(1, std::min(need, cap));
+}
+
+// ------------------------------------------------------------- launches -----
+struct Scratch {
+  double2* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b) {
+    if (b <= bytes) return;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    bytes = 0;
+    CK(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+size_t conv_scratch_bytes(const AxisPlan& ap, long long lines) {
+  const size_t sm = smem_conv(ap);
+  const int grid = grid_for(ap.k->conv_fn, ap.k, sm, lines);
+  return (size_t)grid * ap.k->G * ap.dev.S * sizeof(double2);
+}
+
+void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, const double2* g, double2* out,
+                 Scratch& scratch, cudaStream_t s) {
+  if (lin.count == 0) return;
+  const size_t sm = smem_conv(ap);
+  const int grid = grid_for(ap.k->conv_fn, ap.k, sm, lin.count);
+  scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
+  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p};
+  ap.k->conv(a, grid, sm, s);
+  CK(cudaGetLastError());
+}
+
+void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
+                int ref_order, cudaStream_t s) {
+  if (lin.count == 0) return;
+  const size_t sm = smem_fwd(ap);
+  const int grid = grid_for(ap.k->fwd_fn, ap.k, sm, lin.count);
+  hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+  ap.k->fwd(a, grid, sm, s);
+  CK(cudaGetLastError());
+}
+
+void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
+                const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
+  if (lin.count == 0) return;
+  const size_t sm = smem_bwd(ap);
+  const int grid = grid_for(ap.k->bwd_fn, ap.k, sm, lin.count);
+  hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+  ap.k->bwd(a, grid, sm, s);
+  CK(cudaGetLastError());
+}
+
+// --------------------------------------------------------- synthetic data ---
+__device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_fill_uniform(unsigned long long seed, unsigned long long a, unsigned long long first, long long n,
+                               double2* out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const unsigned long long idx = first + (unsigned long long)i;
+    double v[2];
+    for (unsigned long long comp = 0; comp < 2; ++comp) {
+      const unsigned long long z = mix64(seed * 0x9E3779B97F4A7C15ull + ((a << 56) | (comp << 55) | idx));
+      v[comp] = 2.0 * ((double)(z >> 11) * 0x1.0p-53) - 1.0;
+    }
+    out[i] = make_double2(v[0], v[1]);
+  }
+}
+
+// ------------------------------------------------------------- planner ------
+bool smooth7(size_t m) {
+  for (size_t f : {2, 3, 5, 7})
+    while (m % f == 0) m /= f;
+  return m == 1;
+}
+
+struct Candidate {
+  size_t m;
+  hb::PlanParams pp;
+  double ms = 0;
+};
+
+// Candidate m values: 7-smooth sizes whose block length has a radix kernel
+// (the direct-sum kernel only for blocks of at most 64 points), deduplicated by the GPU work
+// they imply (block length, block count) keeping the smallest m (SPEC.md:536 tie-break).
+// The explicit candidate p = q = 1 is part of the scan whenever a kernel covers m >= M.
+std::vector<Candidate> plan_candidates(hb::Symmetry sym, size_t L, size_t M) {
+  std::vector<Candidate> out;
+  std::map<std::pair<size_t, size_t>, size_t> seen;
+  const size_t mmax = 4 * M + 8;
+  for (size_t m = 1; m <= mmax; ++m) {
+    if (!smooth7(m)) continue;
+    hb::PlanParams pp = hb::deriveParams(L, M, m, sym);
+    const int Bc = complex_len(pp);
+    const KernelEntry* k = find_kernel((int)sym, Bc, Bc <= 64);
+    if (!k) continue;
+    auto key = std::make_pair(pp.blockLength(), pp.n);
+    if (seen.count(key)) continue;
+    seen[key] = m;
+    out.push_back(Candidate{m, pp, 0});
+  }
+  return out;
+}
+
+std::string plan_cache_key(hb::Symmetry sym, size_t L, size_t M, long long lines) {
+  return dev_info().name + "|" + hb::name(sym) + "|" + std::to_string(L) + "|" + std::to_string(M) + "|" +
+         std::to_string(lines);
+}
+
+struct PlannerCache {
+  std::mutex mu;
+  std::map<std::string, std::pair<size_t, double>> mem;  // key -> (m, median ms)
+  bool loaded = false;
+  std::string path() const {
+    const char* p = std::getenv("HCONV_PLAN_CACHE");
+    return p ? std::string(p) : std::string();
+  }
+  void load() {
+    if (loaded) return;
+    loaded = true;
+    const std::string p = path();
+    if (p.empty()) return;
+    FILE* f = std::fopen(p.c_str(), "r");
+    if (!f) return;
+    char line[1024];
+    while (std::fgets(line, sizeof line, f)) {
+      std::string s(line);
+      const size_t a = s.rfind(','), b = s.rfind(',', a - 1);
+      if (a == std::string::npos || b == std::string::npos) continue;
+      mem[s.substr(0, b)] = {std::strtoull(s.c_str() + b + 1, nullptr, 10), std::strtod(s.c_str() + a + 1, nullptr)};
+    }
+    std::fclose(f);
+  }
+  void store(const std::string& key, size_t m, double ms) {
+    mem[key] = {m, ms};
+    const std::string p = path();
+    if (p.empty()) return;
+    if (FILE* f = std::fopen(p.c_str(), "a")) {
+      std::fprintf(f, "%s,%zu,%.6f\n", key.c_str(), m, ms);
+      std::fclose(f);
+    }
+  }
+};
+PlannerCache& planner_cache() {
+  static PlannerCache c;
+  return c;
+}
+
+struct PlanReport {
+  std::vector<Candidate> timed;
+  bool cached = false;
+};
+
+// tune_1d on the device: median of 5 timed runs after one warm-up, CUDA events.
+size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanReport* rep) {
+  auto& cache = planner_cache();
+  const std::string key = plan_cache_key(sym, L, M, lines);
+  {
+    std::lock_guard<std::mutex> lk(cache.mu);
+    cache.load();
+    auto it = cache.mem.find(key);
+    if (it != cache.mem.end()) {
+      if (rep) rep->cached = true;
+      return it->second.first;
+    }
+  }
+  std::vector<Candidate> cands = plan_candidates(sym, L, M);
+  if (cands.empty()) throw Unsupported("planner: no candidate m has a kernel for L=" + std::to_string(L));
+  const size_t data = hb::deriveParams(L, M, 1, sym).dataLength();
+  const size_t elems = (size_t)lines * data;
+  double2 *f = nullptr, *g = nullptr, *o = nullptr;
+  CK(cudaMalloc(&f, elems * sizeof(double2)));
+  CK(cudaMalloc(&g, elems * sizeof(double2)));
+  CK(cudaMalloc(&o, elems * sizeof(double2)));
+  k_fill_uniform<<<256, 256>>>(7, 0, 0, (long long)elems, f);
+  k_fill_uniform<<<256, 256>>>(7, 1, 0, (long long)elems, g);
+  CK(cudaGetLastError());
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  Scratch scratch;
+  const hc::Lines lin{lines, 1, (long long)data, 0, 1};
+  size_t best = 0;
+  double best_ms = 1e30;
+  for (auto& c : cands) {
+    AxisPlan ap = make_axis(c.pp);
+    launch_conv(ap, lin, f, g, o, scratch, 0);
+    std::vector<double> t;
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaEventRecord(e0));
+      launch_conv(ap, lin, f, g, o, scratch, 0);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      t.push_back(ms);
+    }
+    std::sort(t.begin(), t.end());
+    c.ms = t[2];
+    if (c.ms < best_ms * (1 - 1e-9)) {  // strict improvement; ties keep the smaller m
+      best_ms = c.ms;
+      best = c.m;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  scratch.release();
+  cudaFree(f);
+  cudaFree(g);
+  cudaFree(o);
+  if (rep) rep->timed = cands;
+  std::lock_guard<std::mutex> lk(cache.mu);
+  cache.store(key, best, best_ms);
+  return best;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ plan ----
+struct hconv_plan {
+  hconv_desc d{};
+  int device = 0;
+  std::vector<AxisPlan> ax;
+  Scratch scratch;                    // conv1d accumulator slots
+  std::vector<double2*> buffers;      // N-D work / accumulator buffers
+  std::vector<size_t> level_work, level_acc;  // per level: elements of one work buffer / acc
+  PlanReport report;
+  ~hconv_plan() {
+    scratch.release();
+    for (double2* b : buffers)
+      if (b) cudaFree(b);
+  }
+};
+
+namespace {
+
+// N-D: arrays at a level are contiguous with extents data[level..d-1].
+size_t inner_elems(const hconv_plan* P, int level) {
+  size_t x = 1;
+  for (size_t k = level + 1; k < P->ax.size(); ++k) x *= P->ax[k].data;
+  return x;
+}
+
+// buffers layout: for level l < d-1: A work buffers then one accumulator
+double2* level_work(hconv_plan* P, int level, int a) { return P->buffers[level * (P->d.A + 1) + a]; }
+double2* level_acc(hconv_plan* P, int level) { return P->buffers[level * (P->d.A + 1) + P->d.A]; }
+
+// convolve_nd as grid-wide passes: for each outer residue v, forward the
+// outer axis of every column into work buffers, convolve the spectral lines recursively
+// (in place into work[0]), inverse the outer axis and accumulate (one normalisation per axis).
+void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, double2* out, cudaStream_t s) {
+  const int d = (int)P->ax.size();
+  const AxisPlan& ap = P->ax[level];
+  const long long inner = (long long)inner_elems(P, level);
+  const long long Lx = (long long)ap.data, asz = Lx * inner;
+  if (level == d - 1) {
+    const hc::Lines lin{NB, 1, asz, 0, 1};
+    launch_conv(ap, lin, in[0], in[1], out, P->scratch, s);
+    return;
+  }
+  const long long B = ap.dev.B, n = ap.dev.n;
+  const hc::Lines cols{NB * inner, inner, asz, 1, inner};       // columns of the input arrays
+  const hc::Lines wcols{NB * inner, inner, B * inner, 1, inner};  // columns of the work arrays
+  double2* acc = level_acc(P, level);
+  std::vector<const double2*> sub(P->d.A);
+  for (size_t a = 0; a < P->d.A; ++a) sub[a] = level_work(P, level, (int)a);
+  const double scale = 1.0 / (double)ap.dev.qm;
+  for (int v = 0; v < n; ++v) {
+    for (size_t a = 0; a < P->d.A; ++a) launch_fwd(ap, cols, wcols, in[a], level_work(P, level, (int)a), v, 0, s);
+    nd_level(P, level + 1, NB * B, sub.data(), level_work(P, level, 0), s);
+    const bool first = v == 0, last = v == n - 1;
+    double2* dst = last ? out : acc;
+    const double2* accsrc = first ? nullptr : acc;
+    launch_bwd(ap, wcols, cols, level_work(P, level, 0), dst, accsrc, last ? scale : 1.0, v, 0, s);
+  }
+}
+
+void check_desc(const hconv_desc* d) {
+  if (!d) throw std::invalid_argument("null descriptor");
+  if (d->dims < 1 || d->dims > 3) throw std::invalid_argument("dims must be 1, 2 or 3");
+  if (d->mult != HCONV_MULT_PRODUCT) throw std::invalid_argument("unknown multiplication operator");
+  if (d->A != 2 || d->B != 1) throw Unsupported("builtin product kernels are binary: A == 2, B == 1");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hconv_backend(void) { return "cuda-sm_100a"; }
+const char* hconv_last_error(void) { return g_err.c_str(); }
+
+static void to_abi(const hb::PlanParams& pp, hconv_params* o) {
+  o->L = pp.L; o->M = pp.M; o->m = pp.m; o->p = pp.p; o->q = pp.q; o->n = pp.n;
+  o->D = pp.D; o->C = pp.C; o->S = pp.S; o->inplace = pp.inplace ? 1 : 0;
+  o->symmetry = (int)pp.symmetry; o->regime = (int)pp.regime;
+}
+static hb::PlanParams from_abi(const hconv_params* a) {
+  if (!a) throw std::invalid_argument("null params");
+  hb::PlanParams pp = hb::deriveParams(a->L, a->M, a->m, to_sym(a->symmetry));
+  pp.C = a->C ? a->C : 1;
+  pp.S = a->S ? a->S : 1;
+  pp.D = a->D ? a->D : 1;
+  pp.inplace = a->inplace != 0;
+  return pp;
+}
+
+hconv_status hconv_derive_params(size_t L, size_t M, size_t m, int sym, hconv_params* out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null output");
+    to_abi(hb::deriveParams(L, M, m, to_sym(sym)), out);
+  });
+}
+size_t hconv_block_length(const hconv_params* pp) {
+  try { return from_abi(pp).blockLength(); } catch (...) { return 0; }
+}
+size_t hconv_stored_length(const hconv_params* pp) {
+  try { return from_abi(pp).storedLength(); } catch (...) { return 0; }
+}
+size_t hconv_padded_length(const hconv_params* pp) {
+  try { return from_abi(pp).paddedLength(); } catch (...) { return 0; }
+}
+hconv_status hconv_root(size_t N, int64_t k, double* re, double* im) {
+  return guarded([&] {
+    const hb::Complex z = hb::root(N, k);
+    *re = z.real();
+    *im = z.imag();
+  });
+}
+hconv_status hconv_work_memory_words(const hconv_params* pp, size_t A, size_t B, size_t d, size_t L, uint64_t* iw,
+                                     double* ew) {
+  return guarded([&] {
+    const hb::WorkEstimate w = hb::workMemoryWords(from_abi(pp), A, B, d, L);
+    *iw = w.implicitWords;
+    *ew = w.explicitWords;
+  });
+}
+hconv_status hconv_root_table(size_t N, double* out) {
+  return guarded([&] {
+    hb::RootTable t(N);
+    for (size_t k = 0; k < N; ++k) {
+      out[2 * k] = t.values()[k].real();
+      out[2 * k + 1] = t.values()[k].imag();
+    }
+  });
+}
+const char* hconv_symmetry_name(int s) {
+  if (s < 0 || s > 2) return "?";
+  return hb::name(static_cast<hb::Symmetry>(s));
+}
+hconv_status hconv_symmetry_from_name(const char* n, int* s) {
+  return guarded([&] { *s = (int)hb::symmetryFromName(n ? n : ""); });
+}
+
+hconv_status hconv_pfft_forward(const hconv_params* pp, const void* f, size_t dist, size_t residue, void* F,
+                                void* stream) {
+  return guarded([&] {
+    const hb::PlanParams p = from_abi(pp);
+    if (residue >= p.n) throw std::invalid_argument("residue out of range");
+    AxisPlan ap = make_axis(p);
+    const long long bl = (long long)p.blockLength();
+    const hc::Lines lin{(long long)p.C, 1, (long long)dist, 0, (long long)p.S};
+    const hc::Lines lout{(long long)p.C, 1, bl, 0, 1};
+    launch_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 1, (cudaStream_t)stream);
+  });
+}
+hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t residue, void* h, size_t dist,
+                                 int accumulate, void* stream) {
+  return guarded([&] {
+    const hb::PlanParams p = from_abi(pp);
+    if (residue >= p.n) throw std::invalid_argument("residue out of range");
+    AxisPlan ap = make_axis(p);
+    const long long bl = (long long)p.blockLength();
+    const hc::Lines lin{(long long)p.C, 1, bl, 0, 1};
+    const hc::Lines lout{(long long)p.C, 1, (long long)dist, 0, (long long)p.S};
+    launch_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, 1.0, (int)residue, 1,
+               (cudaStream_t)stream);
+  });
+}
+
+hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
+  return guarded([&] {
+    check_desc(desc);
+    if (!out) throw std::invalid_argument("null output");
+    CK(cudaSetDevice(desc->device));
+    auto P = std::make_unique<hconv_plan>();
+    P->d = *desc;
+    P->device = desc->device;
+    const int d = desc->dims;
+    const bool herm = desc->axis[d - 1].symmetry == HCONV_HERMITIAN;
+    // data extents first (needed for per-axis tuning batch sizes)
+    std::vector<size_t> data(d);
+    std::vector<hb::Symmetry> syms(d);
+    for (int k = 0; k < d; ++k) {
+      int s = desc->axis[k].symmetry;
+      if (herm && k < d - 1) s = HCONV_CENTERED;  // outer axes of a Hermitian convolution
+      syms[k] = to_sym(s);
+      data[k] = hb::deriveParams(desc->axis[k].L, desc->axis[k].M, 1, syms[k]).dataLength();
+    }
+    for (int k = 0; k < d; ++k) {
+      const hconv_axis& a = desc->axis[k];
+      size_t m = a.m;
+      if (m == 0) {
+        long long lines = 1;
+        if (d == 1) lines = (long long)(desc->C ? desc->C : 1);
+        else
+          for (int j = 0; j < d; ++j)
+            if (j != k) lines *= (long long)data[j];
+        lines = std::min<long long>(lines, 2048);
+        m = tune_axis(syms[k], a.L, a.M, lines, &P->report);
+      }
+      P->ax.push_back(make_axis(hb::deriveParams(a.L, a.M, m, syms[k])));
+    }
+    if (d == 1) {
+      P->ax[0].pp.C = desc->C ? desc->C : 1;
+    } else {
+      long long NB = 1;
+      for (int l = 0; l < d - 1; ++l) {
+        const long long inner = (long long)inner_elems(P.get(), l);
+        const long long work = NB * P->ax[l].dev.B * inner, acc = NB * (long long)P->ax[l].data * inner;
+        for (size_t a = 0; a < desc->A; ++a) {
+          double2* b = nullptr;
+          CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
+          P->buffers.push_back(b);
+        }
+        double2* b = nullptr;
+        CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
+        P->buffers.push_back(b);
+        NB *= P->ax[l].dev.B;
+      }
+    }
+    *out = P.release();
+  });
+}
+
+hconv_status hconv_plan_params(const hconv_plan* p, int axis, hconv_params* o) {
+  return guarded([&] {
+    if (!p || !o || axis < 0 || axis >= (int)p->ax.size()) throw std::invalid_argument("bad axis");
+    to_abi(p->ax[axis].pp, o);
+  });
+}
+
+size_t hconv_plan_workspace_bytes(const hconv_plan* p) {
+  if (!p) return 0;
+  size_t b = p->scratch.bytes;
+  if (p->d.dims > 1) {
+    long long NB = 1;
+    const int d = p->d.dims;
+    for (int l = 0; l < d - 1; ++l) {
+      size_t inner = 1;
+      for (int k = l + 1; k < d; ++k) inner *= p->ax[k].data;
+      b += (size_t)NB * (p->ax[l].dev.B * p->d.A + p->ax[l].data) * inner * sizeof(double2);
+      NB *= p->ax[l].dev.B;
+    }
+  }
+  return b;
+}
+
+hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* out, void* stream) {
+  return guarded([&] {
+    if (!p || !in || !out || !in[0] || !in[1] || !out[0]) throw std::invalid_argument("null argument");
+    CK(cudaSetDevice(p->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const double2* ins[2] = {(const double2*)in[0], (const double2*)in[1]};
+    if (p->d.dims == 1) {
+      const AxisPlan& ap = p->ax[0];
+      const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
+      const hc::Lines lin{(long long)(p->d.C ? p->d.C : 1), 1, dist, 0, 1};
+      launch_conv(ap, lin, ins[0], ins[1], (double2*)out[0], p->scratch, s);
+    } else {
+      nd_level(p, 0, 1, ins, (double2*)out[0], s);
+    }
+  });
+}
+
+hconv_status hconv_plan_destroy(hconv_plan* p) {
+  delete p;
+  return HCONV_OK;
+}
+
+// ---- utilities outside the reference API (bench / tests) ----
+hconv_status hconv_util_fill_uniform(uint64_t seed, uint64_t a, uint64_t first_index, size_t count, void* out,
+                                     void* stream) {
+  return guarded([&] {
+    if (count == 0) return;
+    const int blocks = (int)std::min<size_t>((count + 255) / 256, 4096);
+    k_fill_uniform<<<blocks, 256, 0, (cudaStream_t)stream>>>(seed, a, first_index, (long long)count, (double2*)out);
+    CK(cudaGetLastError());
+  });
+}
+
+// planner report: up to cap candidates as (m, p, q, n, block, median ms); returns the count
+int hconv_plan_report(const hconv_plan* p, double* out, int cap) {
+  if (!p) return 0;
+  int k = 0;
+  for (const auto& c : p->report.timed) {
+    if (k >= cap) break;
+    double* r = out + 6 * k++;
+    r[0] = (double)c.m; r[1] = (double)c.pp.p; r[2] = (double)c.pp.q; r[3] = (double)c.pp.n;
+    r[4] = (double)c.pp.blockLength(); r[5] = c.ms;
+  }
+  return p->report.cached ? -k - 1 : k;
+}
+
+// kernel description for a plan axis: threads per line group, groups per CTA, radix plan
+const char* hconv_plan_kernel(const hconv_plan* p, int axis) {
+  if (!p || axis < 0 || axis >= (int)p->ax.size()) return "";
+  return p->ax[axis].k->radix;
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// registry.cuh — kernel instantiations available to the host (one table per symmetry).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "naive.cuh"
+
+namespace hc {
+
+struct KernelEntry {
+  int Bc = 0;      // complex FFT length (0 for the naive entry: any length <= kNaiveMax)
+  int T = 0, G = 0;
+  bool naive = false;
+  size_t smem_conv = 0, smem_fwd = 0, smem_bwd = 0;  // per CTA (naive: per complex point)
+  const void* conv_fn = nullptr;
+  const void* fwd_fn = nullptr;
+  const void* bwd_fn = nullptr;
+  void (*conv)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  void (*fwd)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  void (*bwd)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  const char* radix = "";
+};
+
+template <int SYM, class Cfg, int G>
+KernelEntry make_entry(const char* radix) {
+  constexpr bool SR = Cfg::E <= 16;
+  KernelEntry e;
+  e.Bc = Cfg::N;
+  e.T = Cfg::T;
+  e.G = G;
+  e.radix = radix;
+  e.smem_conv = (size_t)G * (Cfg::XS + (SR ? 0 : Cfg::N)) * sizeof(double2);
+  e.smem_fwd = e.smem_bwd = (size_t)G * Cfg::XS * sizeof(double2);
+  e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR>;
+  e.fwd_fn = (const void*)k_pfft_fwd<SYM, Cfg, G>;
+  e.bwd_fn = (const void*)k_pfft_bwd<SYM, Cfg, G>;
+  e.conv = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_conv1d<SYM, Cfg, G, SR><<<grid, Cfg::T * G, sm, s>>>(a);
+  };
+  e.fwd = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_pfft_fwd<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
+  };
+  e.bwd = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_pfft_bwd<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
+  };
+  return e;
+}
+
+template <int SYM>
+KernelEntry make_naive_entry() {
+  KernelEntry e;
+  e.Bc = 0;
+  e.T = kNaiveT;
+  e.G = 1;
+  e.naive = true;
+  e.radix = "direct";
+  e.smem_conv = 3 * sizeof(double2);
+  e.smem_fwd = 1 * sizeof(double2);
+  e.smem_bwd = 2 * sizeof(double2);
+  e.conv_fn = (const void*)k_conv1d_naive<SYM>;
+  e.fwd_fn = (const void*)k_pfft_fwd_naive<SYM>;
+  e.bwd_fn = (const void*)k_pfft_bwd_naive<SYM>;
+  e.conv = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) { k_conv1d_naive<SYM><<<grid, kNaiveT, sm, s>>>(a); };
+  e.fwd = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) { k_pfft_fwd_naive<SYM><<<grid, kNaiveT, sm, s>>>(a); };
+  e.bwd = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) { k_pfft_bwd_naive<SYM><<<grid, kNaiveT, sm, s>>>(a); };
+  return e;
+}
+
+// Radix plans (complex FFT length -> passes, threads per line group, groups per CTA).
+template <int SYM>
+inline void build_registry(KernelEntry* out, int* count) {
+  int k = 0;
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4>("8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4>("16x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4>("4x8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, 2>("8x8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, 2>("16x16x4");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1>("16x16x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1>("16x16x16");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
+  out[k++] = make_naive_entry<SYM>();
+  *count = k;
+}
+
+}  // namespace hc

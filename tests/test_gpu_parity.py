@@ -1,0 +1,354 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the CPU oracle on the same seeded
+inputs.  Bar (BASELINE.json north_star): relative L2 <= 1e-12 and, per copy,
+max-abs <= 1e-10 * ||f|| ||g||.  Residue-level tests use 1e-12 relative to the block norm."""
+import math
+
+import numpy as np
+import pytest
+
+from oracle_lib import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-12
+ABS = 1e-10
+
+
+def _t(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def _rand(rng, shape):
+    return rng.uniform(-1, 1, shape) + 1j * rng.uniform(-1, 1, shape)
+
+
+def _check_conv(h, ref, f, g, axis=-1):
+    assert rel_l2(h, ref) <= REL, rel_l2(h, ref)
+    # per copy max-abs bound
+    fn = np.sqrt((np.abs(f) ** 2).sum(axis=axis))
+    gn = np.sqrt((np.abs(g) ** 2).sum(axis=axis))
+    err = np.abs(h - ref).max(axis=axis)
+    assert np.all(err <= ABS * fn * gn + 1e-300), float((err / (fn * gn)).max())
+
+
+# ---------------------------------------------------------------- fill / inputs --
+def test_fill_uniform_matches_oracle(cuda, oracle):
+    import torch
+
+    t = torch.empty(10000, dtype=torch.complex128, device="cuda")
+    cuda.fill_uniform(t, 1, 0, first_index=123)
+    ref = oracle.uniform(1, 0, 10000, first=123)
+    np.testing.assert_array_equal(t.cpu().numpy(), ref)
+    assert np.abs(ref.real).max() <= 1 and np.abs(ref.imag).max() <= 1
+
+
+# -------------------------------------------------------------- residue level ----
+FAST_BC = [64, 128, 256, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144]
+
+
+def _residue_cases():
+    cases = []
+    # small grids through the direct-sum kernels (SPEC.md:223-225 style), all regimes
+    for sym in (0, 1, 2):
+        for L in (1, 2, 3, 5, 6, 7, 10, 11, 19):
+            if sym == 2 and L % 2 == 0:
+                continue
+            for M in sorted({L, 2 * L - 1 if L > 1 else 1, 2 * L, (3 * L + 1) // 2, 3 * L}):
+                if M < L:
+                    continue
+                for m in sorted({1, 2, 3, 4, max(1, L // 2), L, M}):
+                    cases.append((sym, L, M, m))
+    # radix kernels: one case per fast block size and symmetry, p = 1 / p = 2 / inner
+    for Bc in FAST_BC:
+        cases.append((0, Bc - 3, 2 * Bc - 7, Bc))                 # P1, q = 2
+        cases.append((0, Bc + Bc // 2, 3 * Bc, Bc))               # P2
+        if Bc % 4 == 0:
+            cases.append((0, Bc - 1, 2 * Bc - 1, Bc // 4))        # inner p = 4, B = Bc
+        cases.append((1, 2 * Bc - 1, 3 * Bc - 2, Bc))             # centered P2
+        cases.append((2, 4 * Bc - 1, 6 * Bc - 2, 2 * Bc))         # Hermitian P2, B = 2 Bc
+        cases.append((2, 4 * Bc - 3, 6 * Bc, Bc))                 # Hermitian inner p = 4, B = 2 Bc
+    return cases
+
+
+@pytest.mark.parametrize("case", _residue_cases(), ids=lambda c: "s%d_L%d_M%d_m%d" % c)
+def test_residue_forward_backward(cuda, oracle, case):
+    sym, L, M, m = case
+    try:
+        pp = cuda.deriveParams(L, M, m, cuda.Symmetry(sym))
+    except ValueError:
+        pytest.skip("invalid params")
+    op = oracle.derive(L, M, m, sym)
+    rng = np.random.default_rng(L * 1000 + M * 10 + m + sym)
+    S = pp.dataLength()
+    f = _rand(rng, (3, S))
+    if sym == 2:
+        f[:, 0] = f[:, 0].real
+    try:
+        for r in range(pp.n):
+            F = cuda.forward(_t(f), pp, r).cpu().numpy()
+            for c in range(3):
+                ref = oracle.forward(op, f[c], r)
+                assert rel_l2(F[c], ref) <= REL, (r, c, rel_l2(F[c], ref))
+            h = cuda.backward(_t(F), pp, r).cpu().numpy()
+            for c in range(3):
+                ref = oracle.backward(op, F[c], r)
+                assert rel_l2(h[c], ref) <= REL, (r, c, rel_l2(h[c], ref))
+    except NotImplementedError:
+        pytest.skip("no kernel for this block length")
+
+
+# ---------------------------------------------------------------- 1D convolve ----
+def _conv_cases():
+    cases = []
+    for sym in (0, 1, 2):
+        for L in (1, 2, 5, 6, 9, 17, 31):
+            if sym == 2 and L % 2 == 0:
+                continue
+            M = 2 * L - 1 if sym == 0 else (3 * L + 1) // 2
+            M = max(M, L)
+            for m in sorted({1, 2, 3, max(1, L // 3), L, M}):
+                cases.append((sym, L, M, m))
+    for Bc in FAST_BC:
+        cases.append((0, Bc, 2 * Bc - 1, Bc))
+        if Bc % 4 == 0:
+            cases.append((0, Bc - 1, 2 * Bc - 1, Bc // 4))        # inner p = 4
+        cases.append((1, 2 * Bc - 1, 3 * Bc - 2, Bc))
+        cases.append((2, 4 * Bc - 1, 6 * Bc - 2, 2 * Bc))
+    return cases
+
+
+@pytest.mark.parametrize("case", _conv_cases(), ids=lambda c: "s%d_L%d_M%d_m%d" % c)
+def test_conv1d_vs_oracle(cuda, oracle, case):
+    sym, L, M, m = case
+    pp = cuda.deriveParams(L, M, m, cuda.Symmetry(sym))
+    S = pp.dataLength()
+    C_ = 5
+    rng = np.random.default_rng(S + m)
+    f, g = _rand(rng, (C_, S)), _rand(rng, (C_, S))
+    if sym == 2:
+        f[:, 0], g[:, 0] = f[:, 0].real, g[:, 0].real
+    try:
+        plan = cuda.Conv1dPlan(L, M, m, cuda.Symmetry(sym), C_=C_)
+    except NotImplementedError:
+        pytest.skip("no kernel")
+    ft, gt = _t(f), _t(g)
+    out = cuda.convolve([ft, gt], plan.mult, plan, out=ft.clone() * 0)[0].cpu().numpy()
+    ref = np.stack([oracle.convolve([(L, M, m, sym)], f[c], g[c]) for c in range(C_)])
+    _check_conv(out, ref, f, g)
+    # in place (reference convention: result overwrites the first input)
+    cuda.convolve([ft, gt], plan.mult, plan)
+    np.testing.assert_array_equal(ft.cpu().numpy(), out)
+
+
+def test_conv1d_direct_sum_small(cuda, oracle):
+    """SPEC.md:414 Fig.1 geometry and SPEC.md:592 [1,2]*[3,4]."""
+    plan = cuda.Conv1dPlan(6, 11, 4)
+    rng = np.random.default_rng(5)
+    f, g = _rand(rng, (1, 6)), _rand(rng, (1, 6))
+    out = cuda.convolve([_t(f), _t(g)], plan.mult, plan)[0].cpu().numpy()[0]
+    np.testing.assert_allclose(out, np.convolve(f[0], g[0])[:6], rtol=0, atol=1e-13)
+    plan = cuda.Conv1dPlan(2, 3, 2)
+    out = cuda.convolve([_t(np.array([[1, 2]], complex)), _t(np.array([[3, 4]], complex))], plan.mult, plan)[0]
+    np.testing.assert_allclose(out.cpu().numpy()[0], [3, 10], atol=1e-14)
+
+
+# -------------------------------------------------------------- configurations --
+def _inputs(cuda, shape, seed, herm_axes=None):
+    import torch
+
+    f = torch.empty(shape, dtype=torch.complex128, device="cuda")
+    g = torch.empty(shape, dtype=torch.complex128, device="cuda")
+    cuda.fill_uniform(f, seed, 0)
+    cuda.fill_uniform(g, seed, 1)
+    return f, g
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config1_full(cuda, oracle, seed):
+    L, M, C_ = 1024, 2047, 1024
+    f, g = _inputs(cuda, (C_, L), seed)
+    plan = cuda.Conv1dPlan(L, M, None, C_=C_)
+    out = cuda.convolve([f, g], plan.mult, plan, out=f.clone())[0].cpu().numpy()
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    ref = oracle.convolve([(L, M, plan.params.m, 0)], fn, gn, C_=C_)
+    _check_conv(out, ref, fn, gn)
+
+
+@pytest.mark.parametrize("m", [1024, 512, 256, 2048])
+def test_config1_all_regimes(cuda, oracle, m):
+    L, M, C_ = 1024, 2047, 64
+    f, g = _inputs(cuda, (C_, L), 1)
+    plan = cuda.Conv1dPlan(L, M, m, C_=C_)
+    out = cuda.convolve([f, g], plan.mult, plan, out=f.clone())[0].cpu().numpy()
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    ref = oracle.convolve([(L, M, m, 0)], fn, gn, C_=C_)
+    _check_conv(out, ref, fn, gn)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config2_full(cuda, oracle, seed):
+    """L=6000, M=11999, batch 4096, planner-chosen m; oracle on 96 copies spread over the batch."""
+    L, M, C_ = 6000, 11999, 4096
+    f, g = _inputs(cuda, (C_, L), seed)
+    plan = cuda.Conv1dPlan(L, M, None, C_=C_)
+    assert plan.params.q * plan.params.m >= M
+    out = cuda.convolve([f, g], plan.mult, plan, out=f.clone())[0]
+    rows = np.linspace(0, C_ - 1, 96).astype(int)
+    fn, gn, on = f[rows].cpu().numpy(), g[rows].cpu().numpy(), out[rows].cpu().numpy()
+    ref = oracle.convolve([(L, M, plan.params.m, 0)], fn, gn, C_=len(rows))
+    _check_conv(on, ref, fn, gn)
+
+
+@pytest.mark.parametrize("m", [1536, 6144, 3072, 4096, 2048, 1024])
+def test_config2_hybrid_plans(cuda, oracle, m):
+    """every block size the planner may pick for L=6000 (inner p=4 / p=1 / p=2 / p=3 / p=6)."""
+    L, M, C_ = 6000, 11999, 16
+    f, g = _inputs(cuda, (C_, L), 2)
+    plan = cuda.Conv1dPlan(L, M, m, C_=C_)
+    out = cuda.convolve([f, g], plan.mult, plan, out=f.clone())[0].cpu().numpy()
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    ref = oracle.convolve([(L, M, m, 0)], fn, gn, C_=C_)
+    _check_conv(out, ref, fn, gn)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_config3_full(cuda, oracle, seed):
+    """Hermitian K=8192 (L=16383), M=24574, batch 2048; Im f_0 = 0."""
+    K, C_ = 8192, 2048
+    L, M = 2 * K - 1, 3 * K - 2
+    f, g = _inputs(cuda, (C_, K), seed)
+    f[:, 0] = f[:, 0].real.to(f.dtype)
+    g[:, 0] = g[:, 0].real.to(g.dtype)
+    plan = cuda.Conv1dPlan(L, M, None, cuda.Symmetry.Hermitian, C_=C_)
+    out = cuda.convolve([f, g], plan.mult, plan, out=f.clone())[0]
+    rows = np.linspace(0, C_ - 1, 48).astype(int)
+    fn, gn, on = f[rows].cpu().numpy(), g[rows].cpu().numpy(), out[rows].cpu().numpy()
+    ref = oracle.convolve([(L, M, plan.params.m, 2)], fn, gn, C_=len(rows))
+    _check_conv(on, ref, fn, gn)
+    assert np.abs(on[:, 0].imag).max() <= 1e-12 * np.abs(on).max()  # h_0 real
+
+
+def _explicit_2d(f, g, M):
+    import torch
+
+    N = 1 << (M - 1).bit_length()
+    F = torch.fft.fft2(f, s=(N, N))
+    G = torch.fft.fft2(g, s=(N, N))
+    return torch.fft.ifft2(F * G)[: f.shape[0], : f.shape[1]]
+
+
+def test_config4_full_vs_explicit(cuda):
+    """2D 2048^2, M=4095: against an explicitly padded cuFFT route (independent check)."""
+    L, M = 2048, 4095
+    f, g = _inputs(cuda, (L, L), 1)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(L, M, None), cuda.AxisSpec(L, M, None)])
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=f.clone())[0]
+    ref = _explicit_2d(f, g, M)
+    assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) <= REL
+
+
+@pytest.mark.parametrize("mx,my", [(None, None), (128, 256), (512, 1024)])
+def test_config4_reduced_vs_oracle(cuda, oracle, mx, my):
+    L, M = 256, 511
+    f, g = _inputs(cuda, (L, L), 3)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(L, M, mx), cuda.AxisSpec(L, M, my)])
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=f.clone())[0].cpu().numpy()
+    ref = oracle.convolve([(L, M, plan.params[0].m, 0), (L, M, plan.params[1].m, 0)], f.cpu().numpy(), g.cpu().numpy())
+    assert rel_l2(out, ref) <= REL
+
+
+def _herm3d_inputs(cuda, L, seed):
+    K = (L + 1) // 2
+    f, g = _inputs(cuda, (L, L, K), seed)
+    cuda.hermitian_symmetrize_boundary(f, (L, L, L))
+    cuda.hermitian_symmetrize_boundary(g, (L, L, L))
+    return f, g
+
+
+def _explicit_herm3d(f, g, L, M):
+    """symmetrise the stored half into the full centered cube, explicit cuFFT convolution."""
+    import torch
+
+    H = L // 2
+    K = f.shape[2]
+
+    def full(a):
+        out = torch.zeros((L, L, 2 * K - 1), dtype=a.dtype, device=a.device)
+        out[:, :, K - 1:] = a
+        # f(x, y, -z) = conj f(-x, -y, z): centered stored index i <-> -x at 2H - i
+        out[:, :, : K - 1] = torch.flip(a[:, :, 1:], dims=(0, 1, 2)).conj()
+        return out
+
+    N = M + 2
+    Ff = torch.fft.fftn(full(f), s=(N, N, N))
+    Gf = torch.fft.fftn(full(g), s=(N, N, N))
+    h = torch.fft.ifftn(Ff * Gf)
+    # logical output x in [-H, H] -> index x + 2H (sum of the two offsets), z >= 0 -> z + 2(K-1)
+    xs = torch.arange(-H, L - H, device=f.device) + 2 * H
+    zs = torch.arange(0, K, device=f.device) + 2 * (K - 1)
+    return h[xs][:, xs][:, :, zs]
+
+
+@pytest.mark.slow
+def test_config5_full_vs_explicit(cuda):
+    """3D Hermitian 511^2 x 256 stored, M=766: against an explicitly padded cuFFT route."""
+    L, M = 511, 766
+    f, g = _herm3d_inputs(cuda, L, 1)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(L, M, 256, cuda.Symmetry.Centered), cuda.AxisSpec(L, M, 256, cuda.Symmetry.Centered),
+                            cuda.AxisSpec(L, M, 256, cuda.Symmetry.Hermitian)])
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=f.clone())[0]
+    ref = _explicit_herm3d(f, g, L, M)
+    assert rel_l2(out.cpu().numpy(), ref.cpu().numpy()) <= REL
+
+
+@pytest.mark.parametrize("L,m", [(31, 16), (31, 8), (63, 32), (15, 4)])
+def test_config5_reduced_vs_oracle(cuda, oracle, L, m):
+    M = (3 * L + 1) // 2
+    f, g = _herm3d_inputs(cuda, L, 2)
+    axes = [cuda.AxisSpec(L, M, m, cuda.Symmetry.Centered), cuda.AxisSpec(L, M, m, cuda.Symmetry.Centered),
+            cuda.AxisSpec(L, M, m, cuda.Symmetry.Hermitian)]
+    plan = cuda.ConvPlanND(axes)
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=f.clone())[0].cpu().numpy()
+    ref = oracle.convolve([(L, M, m, 1), (L, M, m, 1), (L, M, m, 2)], f.cpu().numpy(), g.cpu().numpy())
+    assert rel_l2(out, ref) <= REL
+    if L <= 31:
+        ref2 = oracle.direct([1, 1, 2], [L, L, L], f.cpu().numpy(), g.cpu().numpy())
+        assert rel_l2(out, ref2) <= 1e-11
+
+
+def test_symmetrize_matches_oracle(cuda, oracle):
+    import torch
+
+    L = 9
+    f = torch.empty((L, L, 5), dtype=torch.complex128, device="cuda")
+    cuda.fill_uniform(f, 4, 0)
+    ref = oracle.symmetrize([L, L, L], f.cpu().numpy())
+    cuda.hermitian_symmetrize_boundary(f, (L, L, L))
+    np.testing.assert_array_equal(f.cpu().numpy(), ref)
+
+
+def test_planner_picks_valid_plan(cuda):
+    pp, rows, cached = cuda.tune_1d(6000, 11999, cuda.Symmetry.Complex, C_=512)
+    assert pp.q * pp.m >= 11999 and pp.p * pp.m >= 6000
+    if not cached:
+        assert len(rows) >= 2
+        best = min(r["median_ms"] for r in rows)
+        chosen = [r for r in rows if r["m"] == pp.m][0]
+        assert chosen["median_ms"] <= best * 1.0000001
+
+
+def test_errors(cuda):
+    with pytest.raises(ValueError):
+        cuda.deriveParams(0, 4, 2)
+    with pytest.raises(ValueError):
+        cuda.deriveParams(5, 4, 2)
+    with pytest.raises(ValueError):
+        cuda.builtin_mult_product(1)
+    plan = cuda.Conv1dPlan(8, 16, 8, C_=2)
+    import torch
+
+    a = torch.zeros(2, 8, dtype=torch.complex128, device="cuda")
+    with pytest.raises(ValueError):
+        cuda.convolve([a], cuda.builtin_mult_product(2), plan)
