@@ -195,6 +195,14 @@ struct FFTCfg {
     return x;
   }
   static constexpr int XS = X_calc();                                    // exchange buffer (complex)
+  // middle-pass twiddle tables (passes 1..P-2), staged in shared memory:
+  //   MT[MTo(i) + (k-1) * Ns(i+1) + b] = omega_{Ns(i)}^{b k},  1 <= k < R_i,  b < Ns(i+1)
+  static constexpr int MTo(int i) {
+    int o = 0;
+    for (int j = 1; j < i; ++j) o += (RL::R[j] - 1) * Ns(j + 1);
+    return o;
+  }
+  static constexpr int MT = (P > 2) ? MTo(P - 1) : 0;
   static constexpr int ES = C(P - 1) * RL::R[P - 1];                     // last-pass values per thread
 };
 
@@ -206,13 +214,28 @@ struct GroupSync {
   }
 };
 
+// Pass-0 twiddles come from a per-butterfly source p0(beta, t0, w): output k of the pass-0
+// DFT is multiplied by t0 * w^k (w = omega_N^b; t0 folds the residue pre-twiddle
+// zeta_qm^{v b} of the padded transform, or 1).  Passes 1..P-2 read shared-memory tables mt
+// (FFTCfg::MT layout); the last pass has no twiddle.
+template <int DIR, int R, class P0>
+__device__ __forceinline__ void pass0_twiddle(double2* y, int beta, const P0& p0) {
+  double2 t, w;
+  p0(beta, t, w);
+  sfor<R>([&](auto Ki) {
+    constexpr int k = Ki;
+    y[k] = mul_tw<DIR>(y[k], t);
+    if constexpr (k + 1 < R) t = cmul(t, w);
+  });
+}
+
 // Forward FFT: v holds pass-0 inputs (v[c*R0 + a] = x[Ns1*a + b], b = tid + c*T).
 // On return v holds the last pass outputs: v[c*R + k] = X[beta + Rprod(P-1)*k], beta = tid + c*T.
-// tw: zeta_N^e (e < N) in global memory.
-template <class Cfg, int DIR, class Sync>
-__device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* __restrict__ tw,
-                                            int tid, const Sync& sync) {
+template <class Cfg, class Sync, class P0>
+__device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
+                                            const Sync& sync, const P0& p0) {
   constexpr int P = Cfg::P, T = Cfg::T;
+  static_assert(P >= 2, "radix plans have at least two passes");
   sfor<P>([&](auto I) {
     constexpr int i = I;
     constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
@@ -220,12 +243,14 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (NB % T == 0 || beta < NB) {
-        DFT<R, DIR>::run(v + c * R);
-        if constexpr (i < P - 1) {
+        DFT<R, +1>::run(v + c * R);
+        if constexpr (i == 0) {
+          pass0_twiddle<+1, R>(v + c * R, beta, p0);
+        } else if constexpr (i < P - 1) {
           const int b = beta % Ns1;
           sfor<R - 1>([&](auto Ki) {
             constexpr int k = Ki + 1;
-            v[c * R + k] = mul_tw<DIR>(v[c * R + k], __ldg(tw + b * k * Rp));
+            v[c * R + k] = cmul(v[c * R + k], mt[Cfg::MTo(i) + (k - 1) * Ns1 + b]);
           });
         }
       }
@@ -255,24 +280,26 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
   });
 }
 
-// Inverse FFT (DIR = -1 of the forward), starting from the last-pass layout left by
-// fft_forward and ending in the pass-0 layout (v[c*R0 + a] = x[Ns1*a + b]).
-template <class Cfg, class Sync>
-__device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* __restrict__ tw,
-                                            int tid, const Sync& sync) {
+// Inverse FFT (unnormalised, DIR = -1), from the last-pass layout left by fft_forward to the
+// pass-0 layout (v[c*R0 + a] = x[Ns1*a + b]); pass-0 twiddles are the conjugates of p0's.
+template <class Cfg, class Sync, class P0>
+__device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
+                                            const Sync& sync, const P0& p0) {
   constexpr int P = Cfg::P, T = Cfg::T;
   sfor<P>([&](auto Iv) {
     constexpr int i = P - 1 - Iv;
-    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
+    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1);
     sfor<C>([&](auto Ci) {
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (NB % T == 0 || beta < NB) {
-        if constexpr (i < P - 1) {
+        if constexpr (i == 0) {
+          pass0_twiddle<-1, R>(v + c * R, beta, p0);
+        } else if constexpr (i < P - 1) {
           const int b = beta % Ns1;
           sfor<R - 1>([&](auto Ki) {
             constexpr int k = Ki + 1;
-            v[c * R + k] = cmulc(v[c * R + k], __ldg(tw + b * k * Rp));
+            v[c * R + k] = cmulc(v[c * R + k], mt[Cfg::MTo(i) + (k - 1) * Ns1 + b]);
           });
         }
         DFT<R, -1>::run(v + c * R);
@@ -290,7 +317,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
       });
       sync();
       constexpr int R0 = Cfg::R(i - 1), C0 = Cfg::C(i - 1), NB0 = Cfg::NB(i - 1), Rp0 = Cfg::Rprod(i - 1);
-      constexpr int Ns0 = Cfg::Ns(i);  // row length of the exchange
+      constexpr int Ns0 = Cfg::Ns(i);
       sfor<C0>([&](auto Ci) {
         constexpr int c = Ci;
         const int beta = tid + c * T;

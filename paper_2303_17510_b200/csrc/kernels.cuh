@@ -52,7 +52,7 @@ __device__ __forceinline__ bool bvalid(int c, int tid) {
   return NB % Cfg::T == 0 || tid + c * Cfg::T < NB;
 }
 
-// pass-0 load of one input line
+// pass-0 load of one input line (radix kernels: table-driven, no runtime modulo)
 template <int SYM, class Cfg>
 __device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& a, const double2* f, long long es,
                                            int res, int tid) {
@@ -61,10 +61,26 @@ __device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& 
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
     if (bvalid<Cfg, 0>(c, tid)) {
-      sfor<R0>([&](auto Ai) { v[c * R0 + Ai] = load_in<SYM>(a, f, es, Ns1 * Ai + b, res); });
+      sfor<R0>([&](auto Ai) {
+        constexpr int ai = Ai;
+        if constexpr (SYM == SYM_HERMITIAN) v[c * R0 + ai] = load_Zp_fast(a, f, es, Ns1 * ai + b, res, ai, b);
+        else v[c * R0 + ai] = load_fast<SYM>(a, f, es, Ns1 * ai + b, res, ai);
+      });
     }
   });
 }
+
+// pass-0 output twiddle source: omega_Bc^{b k} times (complex / centered) the folded residue
+// factor zeta_qm^{v b}
+template <int SYM>
+struct P0Res {
+  const AxisDev* a;
+  int v;
+  __device__ __forceinline__ void operator()(int b, double2& t, double2& w) const {
+    w = tA(*a, b);
+    t = (SYM != SYM_HERMITIAN && v) ? tZ(*a, v, b) : make_double2(1.0, 0.0);
+  }
+};
 
 // inverse post-processing from pass-0 layout (complex / centered)
 template <int SYM, class Cfg>
@@ -75,7 +91,7 @@ __device__ __forceinline__ void store_pass0(const double2 (&v)[Cfg::E], const Ax
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
     if (bvalid<Cfg, 0>(c, tid)) {
-      sfor<R0>([&](auto Ai) { store_w<SYM>(a, em, Ns1 * Ai + b, res, v[c * R0 + Ai]); });
+      sfor<R0>([&](auto Ai) { store_fast<SYM>(a, em, Ns1 * Ai + b, res, Ai, v[c * R0 + Ai]); });
     }
   });
 }
@@ -91,8 +107,17 @@ __device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const Axi
     if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) { Z[Ns1 * Ai + b] = v[c * R0 + Ai]; });
   });
   sync();
-  for (int j = tid; j < a.S; j += Cfg::T) em(j, herm_w(a, Z, j, res));
+  for (int j = tid; j < a.S; j += Cfg::T) em(j, herm_w_fast<Ns1>(a, Z, j, res));
   sync();
+}
+
+// stage the middle-pass twiddle tables into shared memory (whole CTA)
+template <class Cfg>
+__device__ __forceinline__ void stage_mt(double2* mt, const AxisDev& a) {
+  if constexpr (Cfg::MT > 0) {
+    for (int i = threadIdx.x; i < Cfg::MT; i += blockDim.x) mt[i] = __ldg(a.tab + a.oMT + i);
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------ conv1d --
@@ -103,10 +128,12 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
   constexpr int GS = Cfg::XS + (STASH_REGS ? 0 : Cfg::N);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* X = smem + g * GS;
+  double2* mt = smem;
+  double2* X = smem + Cfg::MT + g * GS;
   double2* stash = X + Cfg::XS;
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
+  stage_mt<Cfg>(mt, a);
   const long long es = p.lin.es;
   double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
@@ -114,8 +141,9 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
     for (int res = 0; res < a.n; ++res) {
       double2 v[Cfg::E];
       double2 Fr[STASH_REGS ? Cfg::E : 1];
+      const P0Res<SYM> p0{&a, res};
       load_pass0<SYM, Cfg>(v, a, p.f + base, es, res, tid);
-      fft_forward<Cfg, +1>(v, X, a.tw, tid, sync);
+      fft_forward<Cfg>(v, X, mt, tid, sync, p0);
       sfor<CL>([&](auto Ci) {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
@@ -125,7 +153,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
           });
       });
       load_pass0<SYM, Cfg>(v, a, p.g + base, es, res, tid);
-      fft_forward<Cfg, +1>(v, X, a.tw, tid, sync);
+      fft_forward<Cfg>(v, X, mt, tid, sync, p0);
       sfor<CL>([&](auto Ci) {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
@@ -138,7 +166,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
             else G_ = cmul(G_, F);
           });
       });
-      fft_inverse<Cfg>(v, X, a.tw, tid, sync);
+      fft_inverse<Cfg>(v, X, mt, tid, sync, p0);
       Emit em;
       const bool last = res == a.n - 1;
       if (last) {
@@ -158,13 +186,16 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {
   extern __shared__ double2 smem[];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* X = smem + g * Cfg::XS;
+  double2* mt = smem;
+  double2* X = smem + Cfg::MT + g * Cfg::XS;
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
+  stage_mt<Cfg>(mt, a);
+  const P0Res<SYM> p0{&a, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
     load_pass0<SYM, Cfg>(v, a, p.f + p.lin.base(item), p.lin.es, p.v, tid);
-    fft_forward<Cfg, +1>(v, X, a.tw, tid, sync);
+    fft_forward<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item), oes = p.lout.es;
     sfor<CL>([&](auto Ci) {
       constexpr int c = Ci;
@@ -194,9 +225,12 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
   extern __shared__ double2 smem[];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* X = smem + g * Cfg::XS;
+  double2* mt = smem;
+  double2* X = smem + Cfg::MT + g * Cfg::XS;
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
+  stage_mt<Cfg>(mt, a);
+  const P0Res<SYM> p0{&a, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
     const long long ib = p.lin.base(item), ies = p.lin.es;
@@ -217,7 +251,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
           }
         });
     });
-    fft_inverse<Cfg>(v, X, a.tw, tid, sync);
+    fft_inverse<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item);
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
     if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, em, p.v, tid, X, sync);

@@ -18,6 +18,8 @@ struct KernelEntry {
   void (*fwd)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   void (*bwd)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   const char* radix = "";
+  int P = 0, R[4] = {0, 0, 0, 0};  // radix plan (host builds the pass-0 / middle-pass tables from it)
+  int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
 };
 
 template <int SYM, class Cfg, int G>
@@ -28,8 +30,11 @@ KernelEntry make_entry(const char* radix) {
   e.T = Cfg::T;
   e.G = G;
   e.radix = radix;
-  e.smem_conv = (size_t)G * (Cfg::XS + (SR ? 0 : Cfg::N)) * sizeof(double2);
-  e.smem_fwd = e.smem_bwd = (size_t)G * Cfg::XS * sizeof(double2);
+  e.smem_conv = (Cfg::MT + (size_t)G * (Cfg::XS + (SR ? 0 : Cfg::N))) * sizeof(double2);
+  e.smem_fwd = e.smem_bwd = (Cfg::MT + (size_t)G * Cfg::XS) * sizeof(double2);
+  e.P = Cfg::P;
+  for (int i = 0; i < Cfg::P; ++i) e.R[i] = Cfg::R(i);
+  e.mt = Cfg::MT;
   e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR>;
   e.fwd_fn = (const void*)k_pfft_fwd<SYM, Cfg, G>;
   e.bwd_fn = (const void*)k_pfft_bwd<SYM, Cfg, G>;
