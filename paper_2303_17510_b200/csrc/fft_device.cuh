@@ -231,9 +231,15 @@ __device__ __forceinline__ void pass0_twiddle(double2* y, int beta, const P0& p0
 
 // Forward FFT: v holds pass-0 inputs (v[c*R0 + a] = x[Ns1*a + b], b = tid + c*T).
 // On return v holds the last pass outputs: v[c*R + k] = X[beta + Rprod(P-1)*k], beta = tid + c*T.
-template <class Cfg, class Sync, class P0>
+struct NoHook {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+// hook() runs right after the last shared-memory exchange (X is free from then on), before the
+// last pass's arithmetic -- used to start the next TMA copy into X early.
+template <class Cfg, class Sync, class P0, class Hook = NoHook>
 __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
-                                            const Sync& sync, const P0& p0) {
+                                            const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
   static_assert(P >= 2, "radix plans have at least two passes");
   sfor<P>([&](auto I) {
@@ -276,15 +282,16 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
         }
       });
       sync();
+      if constexpr (i == P - 2) hook();
     }
   });
 }
 
 // Inverse FFT (unnormalised, DIR = -1), from the last-pass layout left by fft_forward to the
 // pass-0 layout (v[c*R0 + a] = x[Ns1*a + b]); pass-0 twiddles are the conjugates of p0's.
-template <class Cfg, class Sync, class P0>
+template <class Cfg, class Sync, class P0, class Hook = NoHook>
 __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
-                                            const Sync& sync, const P0& p0) {
+                                            const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
   sfor<P>([&](auto Iv) {
     constexpr int i = P - 1 - Iv;
@@ -327,6 +334,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
         }
       });
       sync();
+      if constexpr (i == 1) hook();
     }
   });
 }

@@ -313,20 +313,45 @@ struct Scratch {
   }
 };
 
-size_t conv_scratch_bytes(const AxisPlan& ap, long long lines) {
-  const size_t sm = smem_conv(ap);
-  const int grid = grid_for(ap.k->conv_fn, ap.k, sm, lines);
-  return (size_t)grid * ap.k->G * ap.dev.S * sizeof(double2);
+
+// Staging decision of the radix conv kernel (kernels.cuh): 1 = lines copied by TMA into the
+// exchange buffer, 2 = into a separate buffer, 0 = direct global loads (strided lines, or the
+// line does not fit).  HCONV_NO_STAGE=1 disables staging (A/B measurements).
+struct ConvLayout {
+  int stage = 0, gs = 0, in_off = 0;
+  size_t smem = 0;
+};
+ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
+  ConvLayout c;
+  const KernelEntry* k = ap.k;
+  if (k->naive) {
+    c.smem = smem_conv(ap);
+    return c;
+  }
+  static const bool off = std::getenv("HCONV_NO_STAGE") && std::getenv("HCONV_NO_STAGE")[0] == '1';
+  const int S = ap.dev.S;
+  c.gs = k->xs + k->stash;
+  if (!off && lin.es == 1) {
+    if (S <= k->xs) {
+      c.stage = 1;
+    } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + S)) * sizeof(double2) <= 227 * 1024) {
+      c.stage = 2;
+      c.in_off = c.gs;
+      c.gs += S;
+    }
+  }
+  c.smem = (size_t)(k->mt + (size_t)k->G * c.gs) * sizeof(double2);
+  return c;
 }
 
 void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, const double2* g, double2* out,
                  Scratch& scratch, cudaStream_t s) {
   if (lin.count == 0) return;
-  const size_t sm = smem_conv(ap);
-  const int grid = grid_for(ap.k->conv_fn, ap.k, sm, lin.count);
+  const ConvLayout cl = conv_layout(ap, lin);
+  const int grid = grid_for(ap.k->conv_fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
-  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p};
-  ap.k->conv(a, grid, sm, s);
+  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off};
+  ap.k->conv(a, grid, cl.smem, s);
   CK(cudaGetLastError());
 }
 

@@ -10,6 +10,7 @@
 //  k_pfft_bwd : one residue of backward1/2/Inner[C|H] with accumulation (SPEC pfft-*).
 #pragma once
 #include "block_io.cuh"
+#include "tma.cuh"
 
 namespace hc {
 
@@ -20,6 +21,9 @@ struct ConvArgs {
   const double2* g;
   double2* out;
   double2* scratch;      // per-group accumulator slots (S complex each)
+  int stage;             // 0: pass-0 reads global; 1: lines staged by TMA into X; 2: into a separate buffer
+  int gs;                // group stride in shared memory (complex)
+  int in_off;            // stage 2: offset of the staging buffer inside the group region
 };
 
 struct FwdArgs {
@@ -122,28 +126,61 @@ __device__ __forceinline__ void stage_mt(double2* mt, const AxisDev& a) {
 
 // ------------------------------------------------------------------ conv1d --
 // STASH_REGS: keep the first forward spectrum in registers instead of shared memory.
+// Staged mode (p.stage != 0, unit element stride): every input line (f, g) and the residue
+// accumulator are brought on chip by TMA bulk copies issued one phase ahead -- the next line
+// copy starts as soon as the previous transform has released the exchange buffer, so the
+// HBM/L2 latency overlaps the butterflies of the current transform.
 template <int SYM, class Cfg, int G, bool STASH_REGS>
 __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
-  extern __shared__ double2 smem[];
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2 * G];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
-  constexpr int GS = Cfg::XS + (STASH_REGS ? 0 : Cfg::N);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   double2* mt = smem;
-  double2* X = smem + Cfg::MT + g * GS;
+  double2* X = smem + Cfg::MT + g * p.gs;
   double2* stash = X + Cfg::XS;
+  double2* IN = p.stage == 2 ? X + p.in_off : X;
+  uint64_t* bar_in = &bars[2 * g];
+  uint64_t* bar_acc = &bars[2 * g + 1];
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
   stage_mt<Cfg>(mt, a);
-  const long long es = p.lin.es;
+  const int stage = p.stage;
+  const bool stage_acc = stage != 0 && !STASH_REGS && a.S <= Cfg::N;
+  if (stage && tid == 0) {
+    mbar_init(bar_in, 1);
+    mbar_init(bar_acc, 1);
+    fence_mbar_init();
+  }
+  sync();
+  uint32_t ph_in = 0, ph_acc = 0;
+  const uint32_t row_bytes = (uint32_t)a.S * 16u;
+  const long long es = p.lin.es, step = (long long)gridDim.x * G;
   double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
-  for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
+  long long item = (long long)blockIdx.x * G + g;
+  if (stage && tid == 0 && item < p.lin.count) tma_copy(IN, p.f + p.lin.base(item), row_bytes, bar_in);
+  for (; item < p.lin.count; item += step) {
     const long long base = p.lin.base(item);
     for (int res = 0; res < a.n; ++res) {
+      const bool last = res == a.n - 1;
+      // next f line: the same line for the next residue, else the next item's line
+      const double2* fnext = !last ? p.f + base : (item + step < p.lin.count ? p.f + p.lin.base(item + step) : nullptr);
       double2 v[Cfg::E];
       double2 Fr[STASH_REGS ? Cfg::E : 1];
       const P0Res<SYM> p0{&a, res};
-      load_pass0<SYM, Cfg>(v, a, p.f + base, es, res, tid);
-      fft_forward<Cfg>(v, X, mt, tid, sync, p0);
+      // ---- forward f
+      if (stage) {
+        mbar_wait(bar_in, ph_in);
+        ph_in ^= 1;
+        load_pass0<SYM, Cfg>(v, a, IN, 1, res, tid);
+        sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
+        if (stage == 2 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
+      } else {
+        load_pass0<SYM, Cfg>(v, a, p.f + base, es, res, tid);
+      }
+      fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&] {
+        if (stage == 1 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
+      });
       sfor<CL>([&](auto Ci) {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
@@ -152,7 +189,16 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
             else stash[Ki * NBL + tid + c * T] = v[c * RL + Ki];
           });
       });
-      load_pass0<SYM, Cfg>(v, a, p.g + base, es, res, tid);
+      // ---- forward g
+      if (stage) {
+        mbar_wait(bar_in, ph_in);
+        ph_in ^= 1;
+        load_pass0<SYM, Cfg>(v, a, IN, 1, res, tid);
+        sync();
+        if (stage == 2 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
+      } else {
+        load_pass0<SYM, Cfg>(v, a, p.g + base, es, res, tid);
+      }
       fft_forward<Cfg>(v, X, mt, tid, sync, p0);
       sfor<CL>([&](auto Ci) {
         constexpr int c = Ci;
@@ -166,16 +212,34 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
             else G_ = cmul(G_, F);
           });
       });
-      fft_inverse<Cfg>(v, X, mt, tid, sync, p0);
-      Emit em;
-      const bool last = res == a.n - 1;
-      if (last) {
-        em = Emit{p.out + base, es, res > 0 ? slot : nullptr, 1, 1.0 / (double)a.qm};
-      } else {
-        em = Emit{slot, 1, res > 0 ? slot : nullptr, 1, 1.0};
+      // ---- residue accumulator -> stash (its last reader was the product above)
+      if (stage_acc && res > 0) {
+        sync();
+        if (tid == 0) tma_copy(stash, slot, row_bytes, bar_acc);
       }
-      if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, em, res, tid, X, sync);
-      else store_pass0<SYM, Cfg>(v, a, em, res, tid);
+      // ---- inverse; the next f copy into X starts once X is released (not for the
+      //      Hermitian store, which uses X as its Z buffer)
+      fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&] {
+        if (SYM != SYM_HERMITIAN && stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
+      });
+      const double2* acc = nullptr;
+      if (res > 0) {
+        if (stage_acc) {
+          mbar_wait(bar_acc, ph_acc);
+          ph_acc ^= 1;
+          acc = stash;
+        } else {
+          acc = slot;
+        }
+      }
+      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm} : Emit{slot, 1, acc, 1, 1.0};
+      if constexpr (SYM == SYM_HERMITIAN) {
+        store_herm<Cfg>(v, a, em, res, tid, X, sync);
+        if (stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
+      } else {
+        store_pass0<SYM, Cfg>(v, a, em, res, tid);
+      }
+      if (stage_acc) sync();  // stash (acc) reads done before the next residue stashes F
     }
   }
 }

@@ -20,6 +20,7 @@ struct KernelEntry {
   const char* radix = "";
   int P = 0, R[4] = {0, 0, 0, 0};  // radix plan (host builds the pass-0 / middle-pass tables from it)
   int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
+  int xs = 0, stash = 0;           // exchange buffer / shared-memory stash per group (complex)
 };
 
 template <int SYM, class Cfg, int G>
@@ -35,6 +36,8 @@ KernelEntry make_entry(const char* radix) {
   e.P = Cfg::P;
   for (int i = 0; i < Cfg::P; ++i) e.R[i] = Cfg::R(i);
   e.mt = Cfg::MT;
+  e.xs = Cfg::XS;
+  e.stash = SR ? 0 : Cfg::N;
   e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR>;
   e.fwd_fn = (const void*)k_pfft_fwd<SYM, Cfg, G>;
   e.bwd_fn = (const void*)k_pfft_bwd<SYM, Cfg, G>;
