@@ -45,7 +45,8 @@ struct AxisDev {
   // s = Ns1 a + b (no runtime modulo on the device); see hconv_lib.cu build_tables()
   const double2* tab;
   int ns1, nu, nc;      // Ns1, rows of U (2 R0 + 1), rows of Cv
-  int oZ, oU, oC, oH, oBl, oBh, oMT;
+  int oMT, oU, oC, oA, oZ, oH, oBl, oBh;
+  int tabn;             // entries staged in shared memory (>= the middle-pass tables)
 };
 
 // ---- table accessors (radix kernels) ----
@@ -56,13 +57,19 @@ struct AxisDev {
 //  Hh[v]    = zeta_qm^{v Bc}        (Hermitian)
 //  Bl[b]    = zeta_B^b, Bh[a] = zeta_B^{Ns1 a}   (Hermitian packing)
 //  MT       = middle-pass twiddles (FFTCfg::MT layout)
-__device__ __forceinline__ double2 tA(const AxisDev& a, int b) { return __ldg(a.tab + b); }
-__device__ __forceinline__ double2 tZ(const AxisDev& a, int v, int b) { return __ldg(a.tab + a.oZ + v * a.ns1 + b); }
-__device__ __forceinline__ double2 tU(const AxisDev& a, int v, int i) { return __ldg(a.tab + a.oU + v * a.nu + i); }
-__device__ __forceinline__ double2 tC(const AxisDev& a, int v, int t) { return __ldg(a.tab + a.oC + v * a.nc + t); }
-__device__ __forceinline__ double2 tH(const AxisDev& a, int v) { return __ldg(a.tab + a.oH + v); }
-__device__ __forceinline__ double2 tBl(const AxisDev& a, int b) { return __ldg(a.tab + a.oBl + b); }
-__device__ __forceinline__ double2 tBh(const AxisDev& a, int i) { return __ldg(a.tab + a.oBh + i); }
+// order in memory: MT U C A Z H Bl Bh -- the kernel stages the longest prefix that fits
+// The first a.tabn entries are staged into shared memory at kernel start (tb); the rest, when
+// the shared-memory budget is exhausted, are read through the read-only cache.
+__device__ __forceinline__ double2 tget(const AxisDev& a, const double2* tb, int i) {
+  return i < a.tabn ? tb[i] : __ldg(a.tab + i);
+}
+__device__ __forceinline__ double2 tA(const AxisDev& a, const double2* tb, int b) { return tget(a, tb, a.oA + b); }
+__device__ __forceinline__ double2 tZ(const AxisDev& a, const double2* tb, int v, int b) { return tget(a, tb, a.oZ + v * a.ns1 + b); }
+__device__ __forceinline__ double2 tU(const AxisDev& a, const double2* tb, int v, int i) { return tget(a, tb, a.oU + v * a.nu + i); }
+__device__ __forceinline__ double2 tC(const AxisDev& a, const double2* tb, int v, int t) { return tget(a, tb, a.oC + v * a.nc + t); }
+__device__ __forceinline__ double2 tH(const AxisDev& a, const double2* tb, int v) { return tget(a, tb, a.oH + v); }
+__device__ __forceinline__ double2 tBl(const AxisDev& a, const double2* tb, int b) { return tget(a, tb, a.oBl + b); }
+__device__ __forceinline__ double2 tBh(const AxisDev& a, const double2* tb, int i) { return tget(a, tb, a.oBh + i); }
 
 // zeta_qm^e for |e| < 2^31 (32-bit reduction: exponents are v*j with v < n, |j| < 2B)
 __device__ __forceinline__ double2 zpow(const AxisDev& a, int e) {
@@ -163,64 +170,65 @@ __device__ __forceinline__ double2 herm_w(const AxisDev& a, const double2* Z, in
 // pass-0 element (a, b), s = Ns1 a + b, of residue v, WITHOUT the factor zeta_qm^{v b}
 // (folded into the pass-0 output twiddle t0 = Z[v][b]):  x = zeta_qm^{v Ns1 a} * sum_t ...
 template <int SYM>
-__device__ __forceinline__ double2 load_fast(const AxisDev& a, const double2* __restrict__ f, long long es, int s,
-                                             int v, int ia) {
+__device__ __forceinline__ double2 load_fast(const AxisDev& a, const double2* tb, const double2* __restrict__ f,
+                                             long long es, int s, int v, int ia) {
   double2 x;
   if constexpr (SYM == SYM_COMPLEX) {
     x = s < a.L ? f[(long long)s * es] : make_double2(0.0, 0.0);
     int t = 1;
-    for (int j = s + a.B; j < a.L; j += a.B, ++t) x = cadd(x, v ? cmul(f[(long long)j * es], tC(a, v, t)) : f[(long long)j * es]);
+    for (int j = s + a.B; j < a.L; j += a.B, ++t) x = cadd(x, v ? cmul(f[(long long)j * es], tC(a, tb, v, t)) : f[(long long)j * es]);
   } else {
     x = s < a.L - a.H ? f[(long long)(s + a.H) * es] : make_double2(0.0, 0.0);
     const int st2 = s - a.B + a.H;  // logical s - B
-    if (st2 >= 0) x = cadd(x, v ? cmulc(f[(long long)st2 * es], tC(a, v, 1)) : f[(long long)st2 * es]);
+    if (st2 >= 0) x = cadd(x, v ? cmulc(f[(long long)st2 * es], tC(a, tb, v, 1)) : f[(long long)st2 * es]);
   }
-  return v ? cmul(x, tU(a, v, ia)) : x;
+  return v ? cmul(x, tU(a, tb, v, ia)) : x;
 }
 
 // Hermitian W_s (s in [0, Bc]) with the full factor zeta_qm^{v s} = zs (zeta_qm^{-v B} = conj Cv[v][1]).
-__device__ __forceinline__ double2 load_WH_fast(const AxisDev& a, const double2* __restrict__ f, long long es, int s,
-                                                int v, double2 zs) {
+__device__ __forceinline__ double2 load_WH_fast(const AxisDev& a, const double2* tb, const double2* __restrict__ f,
+                                                long long es, int s, int v, double2 zs) {
   double2 x = s < a.S ? f[(long long)s * es] : make_double2(0.0, 0.0);
   const int r = a.B - s;
-  if (r > 0 && r < a.S) x = cadd(x, v ? cmulc(cconj(f[(long long)r * es]), tC(a, v, 1)) : cconj(f[(long long)r * es]));
+  if (r > 0 && r < a.S) x = cadd(x, v ? cmulc(cconj(f[(long long)r * es]), tC(a, tb, v, 1)) : cconj(f[(long long)r * es]));
   return v ? cmul(x, zs) : x;
 }
 
 // Hermitian packed input Z'_k, k = Ns1 a + b < Bc (no folding into the pass-0 twiddle).
-__device__ __forceinline__ double2 load_Zp_fast(const AxisDev& a, const double2* __restrict__ f, long long es, int k,
-                                                int v, int ia, int b) {
+__device__ __forceinline__ double2 load_Zp_fast(const AxisDev& a, const double2* tb, const double2* __restrict__ f,
+                                                long long es, int k, int v, int ia, int b) {
   double2 zk = make_double2(1.0, 0.0), zm = zk;
   if (v) {
-    zk = cmul(tZ(a, v, b), tU(a, v, ia));   // zeta_qm^{v k}
-    zm = cmulc(tH(a, v), zk);               // zeta_qm^{v (Bc - k)}
+    zk = cmul(tZ(a, tb, v, b), tU(a, tb, v, ia));   // zeta_qm^{v k}
+    zm = cmulc(tH(a, tb, v), zk);               // zeta_qm^{v (Bc - k)}
   }
-  const double2 wk = load_WH_fast(a, f, es, k, v, zk);
-  const double2 wm = cconj(load_WH_fast(a, f, es, a.Bc - k, v, zm));
+  const double2 wk = load_WH_fast(a, tb, f, es, k, v, zk);
+  const double2 wm = cconj(load_WH_fast(a, tb, f, es, a.Bc - k, v, zm));
   const double2 e = cadd(wk, wm);
-  const double2 o = cmul(csub(wk, wm), cmul(tBh(a, ia), tBl(a, b)));  // zeta_B^k
+  const double2 o = cmul(csub(wk, wm), cmul(tBh(a, tb, ia), tBl(a, tb, b)));  // zeta_B^k
   return make_double2(e.x - o.y, e.y + o.x);
 }
 
 // inverse post-processing of pass-0 element s = Ns1 a + b (complex / centered); w already
 // carries conj(Z[v][b]) from the inverse pass-0 twiddle.
 template <int SYM>
-__device__ __forceinline__ void store_fast(const AxisDev& a, const Emit& em, int s, int v, int ia, double2 w) {
-  if (v) w = cmulc(w, tU(a, v, ia));
+__device__ __forceinline__ void store_fast(const AxisDev& a, const double2* tb, const Emit& em, int s, int v, int ia,
+                                           double2 w) {
+  if (v) w = cmulc(w, tU(a, tb, v, ia));
   if constexpr (SYM == SYM_COMPLEX) {
     if (s < a.L) em(s, w);
     int t = 1;
-    for (int j = s + a.B; j < a.L; j += a.B, ++t) em(j, v ? cmulc(w, tC(a, v, t)) : w);
+    for (int j = s + a.B; j < a.L; j += a.B, ++t) em(j, v ? cmulc(w, tC(a, tb, v, t)) : w);
   } else {
     if (s < a.L - a.H) em(s + a.H, w);
     const int st2 = s - a.B + a.H;
-    if (st2 >= 0) em(st2, v ? cmul(w, tC(a, v, 1)) : w);
+    if (st2 >= 0) em(st2, v ? cmul(w, tC(a, tb, v, 1)) : w);
   }
 }
 
 // Hermitian output j in [0, S) from Z (natural order, shared memory); NS1 = Ns1 of the kernel.
 template <int NS1>
-__device__ __forceinline__ double2 herm_w_fast(const AxisDev& a, const double2* Z, int j, int v) {
+__device__ __forceinline__ double2 herm_w_fast(const AxisDev& a, const double2* tb, const double2* Z, int j, int v) {
   const bool hi = j > a.Bc;
   const int k = hi ? a.B - j : j;
   const double2 zk = Z[k == a.Bc ? 0 : k];
@@ -228,9 +236,9 @@ __device__ __forceinline__ double2 herm_w_fast(const AxisDev& a, const double2* 
   const double2 e = cscale(cadd(zk, zm), 0.5);
   const double2 d = cscale(csub(zk, zm), 0.5);
   const double2 o = make_double2(d.y, -d.x);                                   // d / i
-  double2 w = cadd(e, cmulc(o, cmul(tBh(a, k / NS1), tBl(a, k % NS1))));        // e + zeta_B^{-k} o
+  double2 w = cadd(e, cmulc(o, cmul(tBh(a, tb, k / NS1), tBl(a, tb, k % NS1))));        // e + zeta_B^{-k} o
   if (hi) w = cconj(w);
-  return v ? cmulc(w, cmul(tZ(a, v, j % NS1), tU(a, v, j / NS1))) : w;
+  return v ? cmulc(w, cmul(tZ(a, tb, v, j % NS1), tU(a, tb, v, j / NS1))) : w;
 }
 
 // reference order of block value with natural index k' (SPEC pfft-* output: F[u m + l] with

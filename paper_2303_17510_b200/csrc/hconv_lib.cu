@@ -176,6 +176,7 @@ struct AxisPlan {
   hc::AxisDev dev{};
   const KernelEntry* k = nullptr;
   size_t data = 0;  // values per line (dataLength)
+  int tab_full = 0; // table entries the radix kernels use (dev.tabn = the staged prefix)
 };
 
 hb::Symmetry to_sym(int s) {
@@ -201,14 +202,18 @@ void build_tables(AxisPlan& ap) {
   a.ns1 = ns1;
   a.nu = nu;
   a.nc = nc;
-  a.oZ = ns1;
-  a.oU = a.oZ + n * ns1;
+  // order: MT U C A Z H Bl Bh (block_io.cuh); the kernels stage the prefix that fits
+  a.oMT = 0;
+  a.oU = k->mt;
   a.oC = a.oU + n * nu;
-  a.oH = a.oC + n * nc;
+  a.oA = a.oC + n * nc;
+  a.oZ = a.oA + ns1;
+  a.oH = a.oZ + n * ns1;
   a.oBl = a.oH + n;
   a.oBh = a.oBl + ns1;
-  a.oMT = a.oBh + R0 + 1;
-  const int total = a.oMT + k->mt;
+  ap.tab_full = a.sym == hc::SYM_HERMITIAN ? a.oBh + R0 + 1 : a.oH;
+  a.tabn = ap.tab_full;
+  const int total = a.oBh + R0 + 1;
   auto key = std::make_tuple((int)a.Bc, a.qm, a.B, a.n, nc, (const void*)k);
   int d = 0;
   CK(cudaGetDevice(&d));
@@ -228,7 +233,7 @@ void build_tables(AxisPlan& ap) {
     const hb::Complex c = hb::root((size_t)N, e);
     return make_double2(c.real(), c.imag());
   };
-  for (int b = 0; b < ns1; ++b) h[b] = z(Bc, b);
+  for (int b = 0; b < ns1; ++b) h[a.oA + b] = z(Bc, b);
   for (int v = 0; v < n; ++v) {
     for (int b = 0; b < ns1; ++b) h[a.oZ + v * ns1 + b] = z(qm, (long long)v * b);
     for (int i = 0; i < nu; ++i) h[a.oU + v * nu + i] = z(qm, (long long)v * ns1 * i);
@@ -246,7 +251,7 @@ void build_tables(AxisPlan& ap) {
     for (int kk = 1; kk < k->R[i]; ++kk)
       for (long long b = 0; b < Nsi1; ++b) h[o++] = z(Nsi, b * kk);
   }
-  if (o != total) throw std::logic_error("table size mismatch");
+  if (o != a.oU) throw std::logic_error("table size mismatch");
   double2* dp = nullptr;
   CK(cudaMalloc(&dp, (size_t)total * sizeof(double2)));
   CK(cudaMemcpy(dp, h.data(), (size_t)total * sizeof(double2), cudaMemcpyHostToDevice));
@@ -284,8 +289,18 @@ AxisPlan make_axis(const hb::PlanParams& pp, bool allow_naive = true) {
 }
 
 size_t smem_conv(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_conv * ap.dev.Bc : ap.k->smem_conv; }
-size_t smem_fwd(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_fwd * ap.dev.Bc : ap.k->smem_fwd; }
-size_t smem_bwd(const AxisPlan& ap) { return ap.k->naive ? ap.k->smem_bwd * ap.dev.Bc : ap.k->smem_bwd; }
+constexpr size_t kSmemCap = 232448 - 1024;  // opt-in max per block on B200, minus static shared (mbarriers)
+// staged table prefix: everything if it fits next to `group_elems` per group, else at least MT
+int staged_tabn(const AxisPlan& ap, size_t group_elems) {
+  const size_t groups = (size_t)ap.k->G * group_elems;
+  const size_t room = kSmemCap / sizeof(double2) > groups ? kSmemCap / sizeof(double2) - groups : 0;
+  return (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
+}
+size_t smem_fwd(const AxisPlan& ap, int* tabn, bool bwd = false) {
+  if (ap.k->naive) return (bwd ? ap.k->smem_bwd : ap.k->smem_fwd) * ap.dev.Bc;
+  *tabn = staged_tabn(ap, ap.k->xs);
+  return (size_t)(*tabn + (size_t)ap.k->G * ap.k->xs) * sizeof(double2);
+}
 
 int grid_for(const void* fn, const KernelEntry* k, size_t smem, long long items) {
   const int nb = occupancy(fn, k->T * k->G, smem);
@@ -318,7 +333,7 @@ struct Scratch {
 // exchange buffer, 2 = into a separate buffer, 0 = direct global loads (strided lines, or the
 // line does not fit).  HCONV_NO_STAGE=1 disables staging (A/B measurements).
 struct ConvLayout {
-  int stage = 0, gs = 0, in_off = 0;
+  int stage = 0, gs = 0, in_off = 0, tabn = 0;
   size_t smem = 0;
 };
 ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
@@ -334,13 +349,15 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
   if (!off && lin.es == 1) {
     if (S <= k->xs) {
       c.stage = 1;
-    } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + S)) * sizeof(double2) <= 227 * 1024) {
+    } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + S)) * sizeof(double2) <= kSmemCap) {
       c.stage = 2;
       c.in_off = c.gs;
       c.gs += S;
     }
   }
-  c.smem = (size_t)(k->mt + (size_t)k->G * c.gs) * sizeof(double2);
+  c.tabn = staged_tabn(ap, c.gs);
+  c.smem = (size_t)(c.tabn + (size_t)k->G * c.gs) * sizeof(double2);
+  if (c.smem > kSmemCap) throw Unsupported("shared-memory budget exceeded");
   return c;
 }
 
@@ -351,6 +368,7 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   const int grid = grid_for(ap.k->conv_fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
   hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off};
+  a.ax.tabn = cl.tabn;
   ap.k->conv(a, grid, cl.smem, s);
   CK(cudaGetLastError());
 }
@@ -358,9 +376,11 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
 void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
                 int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
-  const size_t sm = smem_fwd(ap);
+  int tabn = 0;
+  const size_t sm = smem_fwd(ap, &tabn);
   const int grid = grid_for(ap.k->fwd_fn, ap.k, sm, lin.count);
   hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+  a.ax.tabn = tabn;
   ap.k->fwd(a, grid, sm, s);
   CK(cudaGetLastError());
 }
@@ -368,9 +388,11 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
 void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
                 const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
-  const size_t sm = smem_bwd(ap);
+  int tabn = 0;
+  const size_t sm = smem_fwd(ap, &tabn, true);
   const int grid = grid_for(ap.k->bwd_fn, ap.k, sm, lin.count);
   hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+  a.ax.tabn = tabn;
   ap.k->bwd(a, grid, sm, s);
   CK(cudaGetLastError());
 }

@@ -58,8 +58,8 @@ __device__ __forceinline__ bool bvalid(int c, int tid) {
 
 // pass-0 load of one input line (radix kernels: table-driven, no runtime modulo)
 template <int SYM, class Cfg>
-__device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& a, const double2* f, long long es,
-                                           int res, int tid) {
+__device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb, const double2* f,
+                                           long long es, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
   sfor<C0>([&](auto Ci) {
     constexpr int c = Ci;
@@ -67,8 +67,8 @@ __device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& 
     if (bvalid<Cfg, 0>(c, tid)) {
       sfor<R0>([&](auto Ai) {
         constexpr int ai = Ai;
-        if constexpr (SYM == SYM_HERMITIAN) v[c * R0 + ai] = load_Zp_fast(a, f, es, Ns1 * ai + b, res, ai, b);
-        else v[c * R0 + ai] = load_fast<SYM>(a, f, es, Ns1 * ai + b, res, ai);
+        if constexpr (SYM == SYM_HERMITIAN) v[c * R0 + ai] = load_Zp_fast(a, tb, f, es, Ns1 * ai + b, res, ai, b);
+        else v[c * R0 + ai] = load_fast<SYM>(a, tb, f, es, Ns1 * ai + b, res, ai);
       });
     }
   });
@@ -79,31 +79,32 @@ __device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& 
 template <int SYM>
 struct P0Res {
   const AxisDev* a;
+  const double2* tb;
   int v;
   __device__ __forceinline__ void operator()(int b, double2& t, double2& w) const {
-    w = tA(*a, b);
-    t = (SYM != SYM_HERMITIAN && v) ? tZ(*a, v, b) : make_double2(1.0, 0.0);
+    w = tA(*a, tb, b);
+    t = (SYM != SYM_HERMITIAN && v) ? tZ(*a, tb, v, b) : make_double2(1.0, 0.0);
   }
 };
 
 // inverse post-processing from pass-0 layout (complex / centered)
 template <int SYM, class Cfg>
-__device__ __forceinline__ void store_pass0(const double2 (&v)[Cfg::E], const AxisDev& a, const Emit& em, int res,
-                                            int tid) {
+__device__ __forceinline__ void store_pass0(const double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb,
+                                            const Emit& em, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
   sfor<C0>([&](auto Ci) {
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
     if (bvalid<Cfg, 0>(c, tid)) {
-      sfor<R0>([&](auto Ai) { store_fast<SYM>(a, em, Ns1 * Ai + b, res, Ai, v[c * R0 + Ai]); });
+      sfor<R0>([&](auto Ai) { store_fast<SYM>(a, tb, em, Ns1 * Ai + b, res, Ai, v[c * R0 + Ai]); });
     }
   });
 }
 
 // Hermitian post-processing: pass-0 layout -> Z in shared memory -> outputs j < S
 template <class Cfg, class Sync>
-__device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const AxisDev& a, const Emit& em, int res,
-                                           int tid, double2* Z, const Sync& sync) {
+__device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb,
+                                           const Emit& em, int res, int tid, double2* Z, const Sync& sync) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
   sfor<C0>([&](auto Ci) {
     constexpr int c = Ci;
@@ -111,17 +112,14 @@ __device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const Axi
     if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) { Z[Ns1 * Ai + b] = v[c * R0 + Ai]; });
   });
   sync();
-  for (int j = tid; j < a.S; j += Cfg::T) em(j, herm_w_fast<Ns1>(a, Z, j, res));
+  for (int j = tid; j < a.S; j += Cfg::T) em(j, herm_w_fast<Ns1>(a, tb, Z, j, res));
   sync();
 }
 
-// stage the middle-pass twiddle tables into shared memory (whole CTA)
-template <class Cfg>
-__device__ __forceinline__ void stage_mt(double2* mt, const AxisDev& a) {
-  if constexpr (Cfg::MT > 0) {
-    for (int i = threadIdx.x; i < Cfg::MT; i += blockDim.x) mt[i] = __ldg(a.tab + a.oMT + i);
-    __syncthreads();
-  }
+// stage the per-axis tables (block_io.cuh: A Z U C MT [H Bl Bh]) into shared memory (whole CTA)
+__device__ __forceinline__ void stage_tables(double2* tb, const AxisDev& a, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tb[i] = __ldg(a.tab + i);
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------ conv1d --
@@ -136,15 +134,16 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
   __shared__ __align__(8) uint64_t bars[2 * G];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* mt = smem;
-  double2* X = smem + Cfg::MT + g * p.gs;
+  double2* tb = smem;
+  const double2* mt = tb;  // middle-pass tables sit at offset 0
+  double2* X = smem + p.ax.tabn + g * p.gs;
   double2* stash = X + Cfg::XS;
   double2* IN = p.stage == 2 ? X + p.in_off : X;
   uint64_t* bar_in = &bars[2 * g];
   uint64_t* bar_acc = &bars[2 * g + 1];
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
-  stage_mt<Cfg>(mt, a);
+  stage_tables(tb, a, a.tabn);
   const int stage = p.stage;
   const bool stage_acc = stage != 0 && !STASH_REGS && a.S <= Cfg::N;
   if (stage && tid == 0) {
@@ -167,16 +166,16 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       const double2* fnext = !last ? p.f + base : (item + step < p.lin.count ? p.f + p.lin.base(item + step) : nullptr);
       double2 v[Cfg::E];
       double2 Fr[STASH_REGS ? Cfg::E : 1];
-      const P0Res<SYM> p0{&a, res};
+      const P0Res<SYM> p0{&a, tb, res};
       // ---- forward f
       if (stage) {
         mbar_wait(bar_in, ph_in);
         ph_in ^= 1;
-        load_pass0<SYM, Cfg>(v, a, IN, 1, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
         sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
         if (stage == 2 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
       } else {
-        load_pass0<SYM, Cfg>(v, a, p.f + base, es, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tb, p.f + base, es, res, tid);
       }
       fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&] {
         if (stage == 1 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
@@ -193,11 +192,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       if (stage) {
         mbar_wait(bar_in, ph_in);
         ph_in ^= 1;
-        load_pass0<SYM, Cfg>(v, a, IN, 1, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
         sync();
         if (stage == 2 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       } else {
-        load_pass0<SYM, Cfg>(v, a, p.g + base, es, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tb, p.g + base, es, res, tid);
       }
       fft_forward<Cfg>(v, X, mt, tid, sync, p0);
       sfor<CL>([&](auto Ci) {
@@ -234,10 +233,10 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       }
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm} : Emit{slot, 1, acc, 1, 1.0};
       if constexpr (SYM == SYM_HERMITIAN) {
-        store_herm<Cfg>(v, a, em, res, tid, X, sync);
+        store_herm<Cfg>(v, a, tb, em, res, tid, X, sync);
         if (stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       } else {
-        store_pass0<SYM, Cfg>(v, a, em, res, tid);
+        store_pass0<SYM, Cfg>(v, a, tb, em, res, tid);
       }
       if (stage_acc) sync();  // stash (acc) reads done before the next residue stashes F
     }
@@ -250,15 +249,16 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {
   extern __shared__ double2 smem[];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* mt = smem;
-  double2* X = smem + Cfg::MT + g * Cfg::XS;
+  double2* tb = smem;
+  const double2* mt = tb;  // middle-pass tables sit at offset 0
+  double2* X = smem + p.ax.tabn + g * Cfg::XS;
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
-  stage_mt<Cfg>(mt, a);
-  const P0Res<SYM> p0{&a, p.v};
+  stage_tables(tb, a, a.tabn);
+  const P0Res<SYM> p0{&a, tb, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
-    load_pass0<SYM, Cfg>(v, a, p.f + p.lin.base(item), p.lin.es, p.v, tid);
+    load_pass0<SYM, Cfg>(v, a, tb, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item), oes = p.lout.es;
     sfor<CL>([&](auto Ci) {
@@ -289,12 +289,13 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
   extern __shared__ double2 smem[];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
-  double2* mt = smem;
-  double2* X = smem + Cfg::MT + g * Cfg::XS;
+  double2* tb = smem;
+  const double2* mt = tb;  // middle-pass tables sit at offset 0
+  double2* X = smem + p.ax.tabn + g * Cfg::XS;
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
-  stage_mt<Cfg>(mt, a);
-  const P0Res<SYM> p0{&a, p.v};
+  stage_tables(tb, a, a.tabn);
+  const P0Res<SYM> p0{&a, tb, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
     const long long ib = p.lin.base(item), ies = p.lin.es;
@@ -318,8 +319,8 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
     fft_inverse<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item);
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
-    if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, em, p.v, tid, X, sync);
-    else store_pass0<SYM, Cfg>(v, a, em, p.v, tid);
+    if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, tb, em, p.v, tid, X, sync);
+    else store_pass0<SYM, Cfg>(v, a, tb, em, p.v, tid);
   }
 }
 
