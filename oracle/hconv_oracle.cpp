@@ -714,8 +714,13 @@ hconv_status hconv_derive_params(size_t L, size_t M, size_t m, int sym, hconv_pa
 size_t hconv_block_length(const hconv_params* pp) {
   try { return block_len(from_abi(pp)); } catch (...) { return 0; }
 }
+// plan.cpp:31-33 (the reference's storage convention; the data convolved per copy is
+// stored_len() = ceil(L/2) values for Hermitian data, the extra entry lies outside the support)
 size_t hconv_stored_length(const hconv_params* pp) {
-  try { return stored_len(from_abi(pp)); } catch (...) { return 0; }
+  try {
+    const Params P = from_abi(pp);
+    return P.sym == HCONV_HERMITIAN ? cq(P.L, 2) + 1 : P.L;
+  } catch (...) { return 0; }
 }
 size_t hconv_padded_length(const hconv_params* pp) { return pp->q * pp->m; }
 hconv_status hconv_root(size_t N, int64_t k, double* re, double* im) {

@@ -126,16 +126,20 @@ __device__ __forceinline__ double2 load_in(const AxisDev& a, const double2* __re
 }
 
 // Destination of residue contributions: dst[j] = ((acc ? acc[j] : 0) + val) * scale.
+// Final outputs are written with the streaming (evict-first) hint so that the L2-resident
+// residue accumulators of the persistent CTAs are not pushed out to HBM.
 struct Emit {
   double2* dst;
   long long des;
   const double2* acc;
   long long aes;
   double scale;
+  bool stream = false;
   __device__ __forceinline__ void operator()(long long j, double2 val) const {
     if (acc) val = cadd(val, acc[j * aes]);
     if (scale != 1.0) val = cscale(val, scale);
-    dst[j * des] = val;
+    if (stream) __stcs(dst + j * des, val);
+    else dst[j * des] = val;
   }
 };
 

@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
           acc = slot;
         }
       }
-      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm} : Emit{slot, 1, acc, 1, 1.0};
+      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
         store_herm<Cfg>(v, a, tb, em, res, tid, X, sync);
         if (stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);

@@ -53,7 +53,7 @@ def load_ref() -> C.CDLL | None:
     lib.ref_derive_params.argtypes = [C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_uint64)]
     lib.ref_lengths.argtypes = [C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(C.c_uint64)]
     lib.ref_root.argtypes = [C.c_size_t, C.c_int64, _dp, _dp]
-    lib.ref_work_memory_words.argtypes = [C.c_size_t] * 7 + [C.POINTER(C.c_uint64), _dp]
+    lib.ref_work_memory_words.argtypes = [C.c_size_t] * 3 + [C.c_int] + [C.c_size_t] * 4 + [C.POINTER(C.c_uint64), _dp]
     lib.ref_root_table.argtypes = [C.c_size_t, C.c_int64, C.c_size_t, _dp]
     lib.ref_root_table_at.argtypes = [C.c_size_t, C.c_uint64, C.c_uint64, _dp, _dp]
     lib.ref_symmetry_name.restype = C.c_char_p
