@@ -136,7 +136,11 @@ struct Emit {
   double scale;
   bool stream = false;
   __device__ __forceinline__ void operator()(long long j, double2 val) const {
-    if (acc) val = cadd(val, acc[j * aes]);
+    put(j, val, acc ? acc[j * aes] : make_double2(0.0, 0.0));
+  }
+  // store with an already-loaded accumulator value (zero when acc == nullptr)
+  __device__ __forceinline__ void put(long long j, double2 val, double2 accv) const {
+    if (acc) val = cadd(val, accv);
     if (scale != 1.0) val = cscale(val, scale);
     if (stream) __stcs(dst + j * des, val);
     else dst[j * des] = val;
@@ -243,6 +247,45 @@ __device__ __forceinline__ double2 herm_w_fast(const AxisDev& a, const double2* 
   double2 w = cadd(e, cmulc(o, cmul(tBh(a, tb, k / NS1), tBl(a, tb, k % NS1))));        // e + zeta_B^{-k} o
   if (hi) w = cconj(w);
   return v ? cmulc(w, cmul(tZ(a, tb, v, j % NS1), tU(a, tb, v, j / NS1))) : w;
+}
+
+// Hermitian post-processing by quads (radix kernels): one (Z_k, Z_{Bc-k}) pair gives
+// w_k, w_{Bc-k} and, by Hermitian symmetry, w_{B-k} = conj w_k and w_{Bc+k} = conj w_{Bc-k}
+// (E_{Bc-k} = conj E_k, O_{Bc-k} = conj O_k, zeta_B^{-(Bc-k)} = -zeta_B^k).  The accumulator
+// values of a quad are loaded before any of its stores.  Bc is even for every radix plan.
+template <int NS1>
+__device__ __forceinline__ void herm_store_quads(const AxisDev& a, const double2* tb, const Emit& em,
+                                                 const double2* Z, int v, int tid, int T) {
+  const int Bc = a.Bc, B = a.B, S = a.S, half = Bc / 2;
+  const double2 one = make_double2(1.0, 0.0);
+  const double2 zBc = v ? tH(a, tb, v) : one;     // zeta_qm^{v Bc}
+  const double2 zB = v ? tC(a, tb, v, 1) : one;   // zeta_qm^{v B}
+  for (int k = tid; k <= half; k += T) {
+    int j[4] = {k, B - k, Bc - k, Bc + k};
+    bool ok[4] = {k < S, k > 0 && B - k < S, Bc - k != k && Bc - k < S, k > 0 && k != half && Bc + k < S};
+    double2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = (ok[u] && em.acc) ? em.acc[j[u] * em.aes] : make_double2(0.0, 0.0);
+    const double2 zk = Z[k];
+    const double2 zm = cconj(Z[k == 0 ? 0 : Bc - k]);
+    const double2 e = cscale(cadd(zk, zm), 0.5);
+    const double2 d = cscale(csub(zk, zm), 0.5);
+    const double2 o = make_double2(d.y, -d.x);                         // d / i
+    const double2 tB = cmul(tBh(a, tb, k / NS1), tBl(a, tb, k % NS1));  // zeta_B^k
+    const double2 wk = cadd(e, cmulc(o, tB));                          // e + zeta_B^{-k} o
+    const double2 wm = csub(cconj(e), cmul(tB, cconj(o)));             // conj e - zeta_B^k conj o
+    double2 w[4] = {wk, cconj(wk), wm, cconj(wm)};
+    if (v) {
+      const double2 zvk = cmul(tZ(a, tb, v, k % NS1), tU(a, tb, v, k / NS1));  // zeta_qm^{v k}
+      w[0] = cmulc(w[0], zvk);                  // zeta^{-v k}
+      w[1] = cmulc(cmul(w[1], zvk), zB);        // zeta^{-v (B - k)}
+      w[2] = cmulc(cmul(w[2], zvk), zBc);       // zeta^{-v (Bc - k)}
+      w[3] = cmulc(cmulc(w[3], zvk), zBc);      // zeta^{-v (Bc + k)}
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (ok[u]) em.put(j[u], w[u], acc[u]);
+  }
 }
 
 // reference order of block value with natural index k' (SPEC pfft-* output: F[u m + l] with

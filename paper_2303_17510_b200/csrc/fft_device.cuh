@@ -20,6 +20,10 @@
 
 #include "tw_consts.h"
 
+// Every lambda on the hot path is force-inlined: the same lambda bodies are shared by several
+// kernels, and an out-of-line call would push the register arrays it touches to local memory.
+#define HC_INL __attribute__((always_inline))
+
 namespace hc {
 
 template <int N, int I = 0, class F>
@@ -86,35 +90,35 @@ struct DFT {
     constexpr int A = first_factor(R);
     if constexpr (A == R) {  // prime: direct sum with compile-time twiddles
       double2 y[R];
-      sfor<R>([&](auto K) {
+      sfor<R>([&](auto K) HC_INL {
         constexpr int k = K;
         double2 acc = x[0];
-        sfor<R - 1>([&](auto J) {
+        sfor<R - 1>([&](auto J) HC_INL {
           constexpr int j = J + 1;
           acc = cadd(acc, twc<R, j * k, DIR>(x[j]));
         });
         y[k] = acc;
       });
-      sfor<R>([&](auto K) { x[K] = y[K]; });
+      sfor<R>([&](auto K) HC_INL { x[K] = y[K]; });
     } else {  // four-step: n = Bf a + b, k = ka + A kb
       constexpr int Bf = R / A;
       double2 t[R];
-      sfor<Bf>([&](auto Bi) {
+      sfor<Bf>([&](auto Bi) HC_INL {
         constexpr int b = Bi;
         double2 y[A];
-        sfor<A>([&](auto Ai) { y[Ai] = x[Bf * Ai + b]; });
+        sfor<A>([&](auto Ai) HC_INL { y[Ai] = x[Bf * Ai + b]; });
         DFT<A, DIR>::run(y);
-        sfor<A>([&](auto Ki) {
+        sfor<A>([&](auto Ki) HC_INL {
           constexpr int ka = Ki;
           t[ka * Bf + b] = twc<R, b * ka, DIR>(y[ka]);
         });
       });
-      sfor<A>([&](auto Ki) {
+      sfor<A>([&](auto Ki) HC_INL {
         constexpr int ka = Ki;
         double2 z[Bf];
-        sfor<Bf>([&](auto Bi) { z[Bi] = t[ka * Bf + Bi]; });
+        sfor<Bf>([&](auto Bi) HC_INL { z[Bi] = t[ka * Bf + Bi]; });
         DFT<Bf, DIR>::run(z);
-        sfor<Bf>([&](auto Kb) { x[ka + A * Kb] = z[Kb]; });
+        sfor<Bf>([&](auto Kb) HC_INL { x[ka + A * Kb] = z[Kb]; });
       });
     }
   }
@@ -222,7 +226,7 @@ template <int DIR, int R, class P0>
 __device__ __forceinline__ void pass0_twiddle(double2* y, int beta, const P0& p0) {
   double2 t, w;
   p0(beta, t, w);
-  sfor<R>([&](auto Ki) {
+  sfor<R>([&](auto Ki) HC_INL {
     constexpr int k = Ki;
     y[k] = mul_tw<DIR>(y[k], t);
     if constexpr (k + 1 < R) t = cmul(t, w);
@@ -242,10 +246,10 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
                                             const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
   static_assert(P >= 2, "radix plans have at least two passes");
-  sfor<P>([&](auto I) {
+  sfor<P>([&](auto I) HC_INL {
     constexpr int i = I;
     constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
-    sfor<C>([&](auto Ci) {
+    sfor<C>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (NB % T == 0 || beta < NB) {
@@ -254,7 +258,7 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
           pass0_twiddle<+1, R>(v + c * R, beta, p0);
         } else if constexpr (i < P - 1) {
           const int b = beta % Ns1;
-          sfor<R - 1>([&](auto Ki) {
+          sfor<R - 1>([&](auto Ki) HC_INL {
             constexpr int k = Ki + 1;
             v[c * R + k] = cmul(v[c * R + k], mt[Cfg::MTo(i) + (k - 1) * Ns1 + b]);
           });
@@ -263,22 +267,92 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
     });
     if constexpr (i < P - 1) {
       constexpr int St = Cfg::St(i + 1);
-      sfor<C>([&](auto Ci) {
+      sfor<C>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
         if (NB % T == 0 || beta < NB) {
           const int K = beta / Ns1, b = beta % Ns1;
-          sfor<R>([&](auto Ki) { X[(K + Rp * Ki) * St + b] = v[c * R + Ki]; });
+          sfor<R>([&](auto Ki) HC_INL { X[(K + Rp * Ki) * St + b] = v[c * R + Ki]; });
         }
       });
       sync();
       constexpr int R2 = Cfg::R(i + 1), C2 = Cfg::C(i + 1), NB2 = Cfg::NB(i + 1), Ns2 = Cfg::Ns(i + 2);
-      sfor<C2>([&](auto Ci) {
+      sfor<C2>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
         if (NB2 % T == 0 || beta < NB2) {
           const int K = beta / Ns2, b = beta % Ns2;
-          sfor<R2>([&](auto Ai) { v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b]; });
+          sfor<R2>([&](auto Ai) HC_INL { v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b]; });
+        }
+      });
+      sync();
+      if constexpr (i == P - 2) hook();
+    }
+  });
+}
+
+// Two independent forward FFTs interleaved pass by pass (v through X, w through Y): half the
+// barrier phases of two separate transforms, and the butterflies of one stream overlap the
+// shared-memory traffic of the other.  hook() runs after the last exchange (X, Y free).
+template <class Cfg, class Sync, class P0, class Hook = NoHook>
+__device__ __forceinline__ void fft_forward_pair(double2 (&v)[Cfg::E], double2 (&w)[Cfg::E], double2* X, double2* Y,
+                                                 const double2* mt, int tid, const Sync& sync, const P0& p0,
+                                                 const Hook& hook = Hook()) {
+  constexpr int P = Cfg::P, T = Cfg::T;
+  static_assert(P >= 2, "radix plans have at least two passes");
+  sfor<P>([&](auto I) HC_INL {
+    constexpr int i = I;
+    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
+    sfor<C>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (NB % T == 0 || beta < NB) {
+        DFT<R, +1>::run(v + c * R);
+        DFT<R, +1>::run(w + c * R);
+        if constexpr (i == 0) {
+          double2 t, tw;
+          p0(beta, t, tw);
+          sfor<R>([&](auto Ki) HC_INL {
+            constexpr int k = Ki;
+            v[c * R + k] = cmul(v[c * R + k], t);
+            w[c * R + k] = cmul(w[c * R + k], t);
+            if constexpr (k + 1 < R) t = cmul(t, tw);
+          });
+        } else if constexpr (i < P - 1) {
+          const int b = beta % Ns1;
+          sfor<R - 1>([&](auto Ki) HC_INL {
+            constexpr int k = Ki + 1;
+            const double2 tw = mt[Cfg::MTo(i) + (k - 1) * Ns1 + b];
+            v[c * R + k] = cmul(v[c * R + k], tw);
+            w[c * R + k] = cmul(w[c * R + k], tw);
+          });
+        }
+      }
+    });
+    if constexpr (i < P - 1) {
+      constexpr int St = Cfg::St(i + 1);
+      sfor<C>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB % T == 0 || beta < NB) {
+          const int K = beta / Ns1, b = beta % Ns1;
+          sfor<R>([&](auto Ki) HC_INL {
+            X[(K + Rp * Ki) * St + b] = v[c * R + Ki];
+            Y[(K + Rp * Ki) * St + b] = w[c * R + Ki];
+          });
+        }
+      });
+      sync();
+      constexpr int R2 = Cfg::R(i + 1), C2 = Cfg::C(i + 1), NB2 = Cfg::NB(i + 1), Ns2 = Cfg::Ns(i + 2);
+      sfor<C2>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB2 % T == 0 || beta < NB2) {
+          const int K = beta / Ns2, b = beta % Ns2;
+          sfor<R2>([&](auto Ai) HC_INL {
+            v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b];
+            w[c * R2 + Ai] = Y[K * St + Ns2 * Ai + b];
+          });
         }
       });
       sync();
@@ -293,10 +367,10 @@ template <class Cfg, class Sync, class P0, class Hook = NoHook>
 __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
                                             const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
-  sfor<P>([&](auto Iv) {
+  sfor<P>([&](auto Iv) HC_INL {
     constexpr int i = P - 1 - Iv;
     constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1);
-    sfor<C>([&](auto Ci) {
+    sfor<C>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (NB % T == 0 || beta < NB) {
@@ -304,7 +378,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
           pass0_twiddle<-1, R>(v + c * R, beta, p0);
         } else if constexpr (i < P - 1) {
           const int b = beta % Ns1;
-          sfor<R - 1>([&](auto Ki) {
+          sfor<R - 1>([&](auto Ki) HC_INL {
             constexpr int k = Ki + 1;
             v[c * R + k] = cmulc(v[c * R + k], mt[Cfg::MTo(i) + (k - 1) * Ns1 + b]);
           });
@@ -314,23 +388,23 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
     });
     if constexpr (i > 0) {
       constexpr int St = Cfg::St(i);
-      sfor<C>([&](auto Ci) {
+      sfor<C>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
         if (NB % T == 0 || beta < NB) {
           const int K = beta / Ns1, b = beta % Ns1;
-          sfor<R>([&](auto Ai) { X[K * St + Ns1 * Ai + b] = v[c * R + Ai]; });
+          sfor<R>([&](auto Ai) HC_INL { X[K * St + Ns1 * Ai + b] = v[c * R + Ai]; });
         }
       });
       sync();
       constexpr int R0 = Cfg::R(i - 1), C0 = Cfg::C(i - 1), NB0 = Cfg::NB(i - 1), Rp0 = Cfg::Rprod(i - 1);
       constexpr int Ns0 = Cfg::Ns(i);
-      sfor<C0>([&](auto Ci) {
+      sfor<C0>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
         if (NB0 % T == 0 || beta < NB0) {
           const int K = beta / Ns0, b = beta % Ns0;
-          sfor<R0>([&](auto Ki) { v[c * R0 + Ki] = X[(K + Rp0 * Ki) * St + b]; });
+          sfor<R0>([&](auto Ki) HC_INL { v[c * R0 + Ki] = X[(K + Rp0 * Ki) * St + b]; });
         }
       });
       sync();

@@ -349,6 +349,8 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
   if (!off && lin.es == 1) {
     if (S <= k->xs) {
       c.stage = 1;
+    } else if (k->pair) {
+      c.stage = 0;  // the paired kernel stages both lines into X and Y or none
     } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + S)) * sizeof(double2) <= kSmemCap) {
       c.stage = 2;
       c.in_off = c.gs;

@@ -61,11 +61,11 @@ template <int SYM, class Cfg>
 __device__ __forceinline__ void load_pass0(double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb, const double2* f,
                                            long long es, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
-  sfor<C0>([&](auto Ci) {
+  sfor<C0>([&](auto Ci) HC_INL {
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
     if (bvalid<Cfg, 0>(c, tid)) {
-      sfor<R0>([&](auto Ai) {
+      sfor<R0>([&](auto Ai) HC_INL {
         constexpr int ai = Ai;
         if constexpr (SYM == SYM_HERMITIAN) v[c * R0 + ai] = load_Zp_fast(a, tb, f, es, Ns1 * ai + b, res, ai, b);
         else v[c * R0 + ai] = load_fast<SYM>(a, tb, f, es, Ns1 * ai + b, res, ai);
@@ -92,11 +92,11 @@ template <int SYM, class Cfg>
 __device__ __forceinline__ void store_pass0(const double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb,
                                             const Emit& em, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
-  sfor<C0>([&](auto Ci) {
+  sfor<C0>([&](auto Ci) HC_INL {
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
     if (bvalid<Cfg, 0>(c, tid)) {
-      sfor<R0>([&](auto Ai) { store_fast<SYM>(a, tb, em, Ns1 * Ai + b, res, Ai, v[c * R0 + Ai]); });
+      sfor<R0>([&](auto Ai) HC_INL { store_fast<SYM>(a, tb, em, Ns1 * Ai + b, res, Ai, v[c * R0 + Ai]); });
     }
   });
 }
@@ -106,13 +106,13 @@ template <class Cfg, class Sync>
 __device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb,
                                            const Emit& em, int res, int tid, double2* Z, const Sync& sync) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
-  sfor<C0>([&](auto Ci) {
+  sfor<C0>([&](auto Ci) HC_INL {
     constexpr int c = Ci;
     const int b = tid + c * Cfg::T;
-    if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) { Z[Ns1 * Ai + b] = v[c * R0 + Ai]; });
+    if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { Z[Ns1 * Ai + b] = v[c * R0 + Ai]; });
   });
   sync();
-  for (int j = tid; j < a.S; j += Cfg::T) em(j, herm_w_fast<Ns1>(a, tb, Z, j, res));
+  herm_store_quads<Ns1>(a, tb, em, Z, res, tid, Cfg::T);
   sync();
 }
 
@@ -167,50 +167,49 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       double2 v[Cfg::E];
       double2 Fr[STASH_REGS ? Cfg::E : 1];
       const P0Res<SYM> p0{&a, tb, res};
-      // ---- forward f
-      if (stage) {
-        mbar_wait(bar_in, ph_in);
-        ph_in ^= 1;
-        load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
-        sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
-        if (stage == 2 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
-      } else {
-        load_pass0<SYM, Cfg>(v, a, tb, p.f + base, es, res, tid);
-      }
-      fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&] {
-        if (stage == 1 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
-      });
-      sfor<CL>([&](auto Ci) {
-        constexpr int c = Ci;
-        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-          sfor<RL>([&](auto Ki) {
-            if constexpr (STASH_REGS) Fr[c * RL + Ki] = v[c * RL + Ki];
-            else stash[Ki * NBL + tid + c * T] = v[c * RL + Ki];
+      // ---- forward padded FFTs of the A = 2 inputs (one code copy: keeps the kernel inside
+      //      the instruction cache); input 0 is stashed, input 1 multiplied by it
+#pragma unroll 1
+      for (int inp = 0; inp < 2; ++inp) {
+        const double2* src = inp == 0 ? p.f : p.g;
+        // TMA issued when this input releases the staging buffer: g after f, then the next f
+        const double2* nxt = inp == 0 ? p.g + base : fnext;
+        if (stage) {
+          mbar_wait(bar_in, ph_in);
+          ph_in ^= 1;
+          load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
+          sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
+          if (stage == 2 && tid == 0 && nxt) tma_copy(IN, nxt, row_bytes, bar_in);
+        } else {
+          load_pass0<SYM, Cfg>(v, a, tb, src + base, es, res, tid);
+        }
+        fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
+          if (stage == 1 && inp == 0 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
+        });
+        if (inp == 0) {
+          sfor<CL>([&](auto Ci) HC_INL {
+            constexpr int c = Ci;
+            if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+              sfor<RL>([&](auto Ki) HC_INL {
+                if constexpr (STASH_REGS) Fr[c * RL + Ki] = v[c * RL + Ki];
+                else stash[Ki * NBL + tid + c * T] = v[c * RL + Ki];
+              });
           });
-      });
-      // ---- forward g
-      if (stage) {
-        mbar_wait(bar_in, ph_in);
-        ph_in ^= 1;
-        load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
-        sync();
-        if (stage == 2 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
-      } else {
-        load_pass0<SYM, Cfg>(v, a, tb, p.g + base, es, res, tid);
-      }
-      fft_forward<Cfg>(v, X, mt, tid, sync, p0);
-      sfor<CL>([&](auto Ci) {
-        constexpr int c = Ci;
-        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-          sfor<RL>([&](auto Ki) {
-            double2 F;
-            if constexpr (STASH_REGS) F = Fr[c * RL + Ki];
-            else F = stash[Ki * NBL + tid + c * T];
-            double2& G_ = v[c * RL + Ki];
-            if constexpr (SYM == SYM_HERMITIAN) G_ = make_double2(G_.x * F.x, G_.y * F.y);  // real residues
-            else G_ = cmul(G_, F);
+        } else {
+          sfor<CL>([&](auto Ci) HC_INL {
+            constexpr int c = Ci;
+            if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+              sfor<RL>([&](auto Ki) HC_INL {
+                double2 F;
+                if constexpr (STASH_REGS) F = Fr[c * RL + Ki];
+                else F = stash[Ki * NBL + tid + c * T];
+                double2& G_ = v[c * RL + Ki];
+                if constexpr (SYM == SYM_HERMITIAN) G_ = make_double2(G_.x * F.x, G_.y * F.y);  // real residues
+                else G_ = cmul(G_, F);
+              });
           });
-      });
+        }
+      }
       // ---- residue accumulator -> stash (its last reader was the product above)
       if (stage_acc && res > 0) {
         sync();
@@ -218,7 +217,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       }
       // ---- inverse; the next f copy into X starts once X is released (not for the
       //      Hermitian store, which uses X as its Z buffer)
-      fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&] {
+      fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
         if (SYM != SYM_HERMITIAN && stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       });
       const double2* acc = nullptr;
@@ -243,6 +242,90 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
   }
 }
 
+// ------------------------------------------------------------- conv1d, paired --
+// For radix plans with at most 16 values per thread: the forward FFTs of f and g run as one
+// interleaved pair (fft_forward_pair) through two exchange buffers X (f) and Y (g); the product
+// needs no stash.  Staging (p.stage == 1): f and g lines are TMA-copied into X and Y; the next
+// g copy starts when the pair releases Y, the next f copy when the inverse releases X.
+template <int SYM, class Cfg, int G>
+__global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2 * G];
+  const int g = threadIdx.x / Cfg::T, tid = threadIdx.x % Cfg::T;
+  double2* tb = smem;
+  const double2* mt = tb;
+  double2* X = smem + p.ax.tabn + g * p.gs;
+  double2* Y = X + Cfg::XS;
+  uint64_t* bar_f = &bars[2 * g];
+  uint64_t* bar_g = &bars[2 * g + 1];
+  const GroupSync sync{g + 1, Cfg::T};
+  const AxisDev& a = p.ax;
+  stage_tables(tb, a, a.tabn);
+  const bool stage = p.stage == 1;
+  if (stage && tid == 0) {
+    mbar_init(bar_f, 1);
+    mbar_init(bar_g, 1);
+    fence_mbar_init();
+  }
+  sync();
+  uint32_t ph_f = 0, ph_g = 0;
+  const uint32_t row_bytes = (uint32_t)a.S * 16u;
+  const long long es = p.lin.es, step = (long long)gridDim.x * G;
+  double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
+  long long item = (long long)blockIdx.x * G + g;
+  if (stage && tid == 0 && item < p.lin.count) {
+    tma_copy(X, p.f + p.lin.base(item), row_bytes, bar_f);
+    tma_copy(Y, p.g + p.lin.base(item), row_bytes, bar_g);
+  }
+  for (; item < p.lin.count; item += step) {
+    const long long base = p.lin.base(item);
+    for (int res = 0; res < a.n; ++res) {
+      const bool last = res == a.n - 1;
+      const bool more = item + step < p.lin.count;
+      const long long nbase = last ? (more ? p.lin.base(item + step) : -1) : base;
+      double2 v[Cfg::E], w[Cfg::E];
+      const P0Res<SYM> p0{&a, tb, res};
+      if (stage) {
+        mbar_wait(bar_f, ph_f);
+        ph_f ^= 1;
+        mbar_wait(bar_g, ph_g);
+        ph_g ^= 1;
+        load_pass0<SYM, Cfg>(v, a, tb, X, 1, res, tid);
+        load_pass0<SYM, Cfg>(w, a, tb, Y, 1, res, tid);
+        sync();
+      } else {
+        load_pass0<SYM, Cfg>(v, a, tb, p.f + base, es, res, tid);
+        load_pass0<SYM, Cfg>(w, a, tb, p.g + base, es, res, tid);
+      }
+      fft_forward_pair<Cfg>(v, w, X, Y, mt, tid, sync, p0, [&]() HC_INL {
+        if (stage && tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+      });
+      constexpr int RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1);
+      sfor<CL>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+          sfor<RL>([&](auto Ki) HC_INL {
+            double2& F = v[c * RL + Ki];
+            const double2 Gv = w[c * RL + Ki];
+            if constexpr (SYM == SYM_HERMITIAN) F = make_double2(F.x * Gv.x, F.y * Gv.y);
+            else F = cmul(F, Gv);
+          });
+      });
+      fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
+        if (SYM != SYM_HERMITIAN && stage && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
+      });
+      const double2* acc = res > 0 ? slot : nullptr;
+      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
+      if constexpr (SYM == SYM_HERMITIAN) {
+        store_herm<Cfg>(v, a, tb, em, res, tid, X, sync);
+        if (stage && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
+      } else {
+        store_pass0<SYM, Cfg>(v, a, tb, em, res, tid);
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pfft fwd --
 template <int SYM, class Cfg, int G>
 __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {
@@ -261,11 +344,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {
     load_pass0<SYM, Cfg>(v, a, tb, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item), oes = p.lout.es;
-    sfor<CL>([&](auto Ci) {
+    sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-        sfor<RL>([&](auto Ki) {
+        sfor<RL>([&](auto Ki) HC_INL {
           const long long kp = beta + (long long)RpL * Ki;
           const double2 val = v[c * RL + Ki];
           if constexpr (SYM == SYM_HERMITIAN) {
@@ -299,11 +382,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
     const long long ib = p.lin.base(item), ies = p.lin.es;
-    sfor<CL>([&](auto Ci) {
+    sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;
       if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-        sfor<RL>([&](auto Ki) {
+        sfor<RL>([&](auto Ki) HC_INL {
           const long long kp = beta + (long long)RpL * Ki;
           if constexpr (SYM == SYM_HERMITIAN) {
             const double* F = (const double*)p.F;
