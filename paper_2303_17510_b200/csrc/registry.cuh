@@ -24,9 +24,11 @@ struct KernelEntry {
   bool pair = false;               // conv kernel is k_conv1d_pair (two exchange buffers per group)
 };
 
-template <int SYM, class Cfg, int G>
+// SMEM_STASH: keep the first spectrum in shared memory even when it would fit in registers
+// (lets G > 1 line groups share an SM within the register budget).
+template <int SYM, class Cfg, int G, bool SMEM_STASH = false>
 KernelEntry make_entry(const char* radix) {
-  constexpr bool SR = Cfg::E <= 16;
+  constexpr bool SR = Cfg::E <= 16 && !SMEM_STASH;
   // paired forward FFTs (k_conv1d_pair) measured slower than the stash path on B200 (r01:
   // c1 0.069 vs 0.057 ms) -- lower occupancy from two exchange buffers; kept selectable.
   constexpr bool PAIR = false;
@@ -94,6 +96,7 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1>("16x16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1>("16x16x16");
+  // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
   out[k++] = make_naive_entry<SYM>();
   *count = k;
