@@ -210,6 +210,11 @@ struct FFTCfg {
   static constexpr int ES = C(P - 1) * RL::R[P - 1];                     // last-pass values per thread
 };
 
+// Whole-CTA barrier (column-tile kernels, whose line groups interleave within warps).
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
 // Group barrier over NT threads (named barrier id; NT must be a multiple of 32).
 struct GroupSync {
   int id, nt;
@@ -241,7 +246,9 @@ struct NoHook {
 
 // hook() runs right after the last shared-memory exchange (X is free from then on), before the
 // last pass's arithmetic -- used to start the next TMA copy into X early.
-template <class Cfg, class Sync, class P0, class Hook = NoHook>
+// XSTR: element stride of the exchange buffer (1, or G when G line groups interleave their
+// buffers element by element -- column-tile kernels, kernels.cuh)
+template <class Cfg, class Sync, class P0, class Hook = NoHook, int XSTR = 1>
 __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
                                             const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
@@ -272,7 +279,7 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
         const int beta = tid + c * T;
         if (NB % T == 0 || beta < NB) {
           const int K = beta / Ns1, b = beta % Ns1;
-          sfor<R>([&](auto Ki) HC_INL { X[(K + Rp * Ki) * St + b] = v[c * R + Ki]; });
+          sfor<R>([&](auto Ki) HC_INL { X[((K + Rp * Ki) * St + b) * XSTR] = v[c * R + Ki]; });
         }
       });
       sync();
@@ -282,7 +289,7 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
         const int beta = tid + c * T;
         if (NB2 % T == 0 || beta < NB2) {
           const int K = beta / Ns2, b = beta % Ns2;
-          sfor<R2>([&](auto Ai) HC_INL { v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b]; });
+          sfor<R2>([&](auto Ai) HC_INL { v[c * R2 + Ai] = X[(K * St + Ns2 * Ai + b) * XSTR]; });
         }
       });
       sync();
@@ -363,7 +370,7 @@ __device__ __forceinline__ void fft_forward_pair(double2 (&v)[Cfg::E], double2 (
 
 // Inverse FFT (unnormalised, DIR = -1), from the last-pass layout left by fft_forward to the
 // pass-0 layout (v[c*R0 + a] = x[Ns1*a + b]); pass-0 twiddles are the conjugates of p0's.
-template <class Cfg, class Sync, class P0, class Hook = NoHook>
+template <class Cfg, class Sync, class P0, class Hook = NoHook, int XSTR = 1>
 __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
                                             const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
   constexpr int P = Cfg::P, T = Cfg::T;
@@ -393,7 +400,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
         const int beta = tid + c * T;
         if (NB % T == 0 || beta < NB) {
           const int K = beta / Ns1, b = beta % Ns1;
-          sfor<R>([&](auto Ai) HC_INL { X[K * St + Ns1 * Ai + b] = v[c * R + Ai]; });
+          sfor<R>([&](auto Ai) HC_INL { X[(K * St + Ns1 * Ai + b) * XSTR] = v[c * R + Ai]; });
         }
       });
       sync();
@@ -404,7 +411,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
         const int beta = tid + c * T;
         if (NB0 % T == 0 || beta < NB0) {
           const int K = beta / Ns0, b = beta % Ns0;
-          sfor<R0>([&](auto Ki) HC_INL { v[c * R0 + Ki] = X[(K + Rp0 * Ki) * St + b]; });
+          sfor<R0>([&](auto Ki) HC_INL { v[c * R0 + Ki] = X[((K + Rp0 * Ki) * St + b) * XSTR]; });
         }
       });
       sync();

@@ -375,9 +375,35 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   CK(cudaGetLastError());
 }
 
+// Column-tile variants for strided outer-axis lines (complex / centered radix kernels).
+bool use_cols(const AxisPlan& ap, const hc::Lines& lin) {
+  static const bool off = std::getenv("HCONV_NO_COLS") && std::getenv("HCONV_NO_COLS")[0] == '1';
+  return !off && !ap.k->naive && ap.k->fwdc && lin.es > 1;
+}
+int cols_tabn(const AxisPlan& ap) {
+  const size_t groups = (size_t)ap.k->gc * ap.k->xs;
+  const size_t room = kSmemCap / sizeof(double2) > groups ? kSmemCap / sizeof(double2) - groups : 0;
+  return (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
+}
+int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items) {
+  const int nb = occupancy(fn, k->T * k->gc, smem);
+  const long long need = (items + k->gc - 1) / k->gc;
+  return (int)std::max<long long>(1, std::min(need, (long long)nb * dev_info().sms));
+}
+
 void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
                 int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  if (use_cols(ap, lin)) {
+    const int tabn = cols_tabn(ap);
+    const size_t sm = (size_t)(tabn + (size_t)ap.k->gc * ap.k->xs) * sizeof(double2);
+    const int grid = grid_cols(ap.k->fwdc_fn, ap.k, sm, lin.count);
+    hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+    a.ax.tabn = tabn;
+    ap.k->fwdc(a, grid, sm, s);
+    CK(cudaGetLastError());
+    return;
+  }
   int tabn = 0;
   const size_t sm = smem_fwd(ap, &tabn);
   const int grid = grid_for(ap.k->fwd_fn, ap.k, sm, lin.count);
@@ -390,6 +416,16 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
 void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
                 const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  if (use_cols(ap, lout)) {
+    const int tabn = cols_tabn(ap);
+    const size_t sm = (size_t)(tabn + (size_t)ap.k->gc * ap.k->xs) * sizeof(double2);
+    const int grid = grid_cols(ap.k->bwdc_fn, ap.k, sm, lin.count);
+    hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+    a.ax.tabn = tabn;
+    ap.k->bwdc(a, grid, sm, s);
+    CK(cudaGetLastError());
+    return;
+  }
   int tabn = 0;
   const size_t sm = smem_fwd(ap, &tabn, true);
   const int grid = grid_for(ap.k->bwd_fn, ap.k, sm, lin.count);

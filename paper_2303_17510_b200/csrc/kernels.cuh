@@ -326,6 +326,86 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
   }
 }
 
+// --------------------------------------------------------- column-tile pfft --
+// Outer-axis passes of the N-D driver read columns at a large element stride.  Here the GC
+// line groups of a CTA take GC ADJACENT columns and interleave thread by thread (thread t ->
+// group t % GC), so every load/store instruction of a warp touches GC consecutive columns
+// (coalesced), and the groups' exchange buffers interleave element by element (conflict-free).
+// Complex / centered data only (Hermitian is always the innermost, contiguous axis).
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols(FwdArgs p) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  double2* tb = smem;
+  const double2* mt = tb;
+  double2* X = smem + p.ax.tabn + g;
+  const CtaSync sync;
+  const AxisDev& a = p.ax;
+  stage_tables(tb, a, a.tabn);
+  const P0Res<SYM> p0{&a, tb, p.v};
+  const long long rounds = (p.lin.count + (long long)gridDim.x * GC - 1) / ((long long)gridDim.x * GC);
+  for (long long rd = 0; rd < rounds; ++rd) {
+    const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
+    const bool live = item < p.lin.count;
+    double2 v[Cfg::E];
+    if (live) load_pass0<SYM, Cfg>(v, a, tb, p.f + p.lin.base(item), p.lin.es, p.v, tid);
+    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X, mt, tid, sync, p0);
+    if (!live) continue;
+    const long long ob = p.lout.base(item), oes = p.lout.es;
+    double2* F = (double2*)p.F;
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL {
+          const long long kp = beta + (long long)RpL * Ki;
+          F[ob + (p.ref_order ? ref_index(a, kp) : kp) * oes] = v[c * RL + Ki];
+        });
+    });
+  }
+}
+
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  double2* tb = smem;
+  const double2* mt = tb;
+  double2* X = smem + p.ax.tabn + g;
+  const CtaSync sync;
+  const AxisDev& a = p.ax;
+  stage_tables(tb, a, a.tabn);
+  const P0Res<SYM> p0{&a, tb, p.v};
+  const long long rounds = (p.lin.count + (long long)gridDim.x * GC - 1) / ((long long)gridDim.x * GC);
+  for (long long rd = 0; rd < rounds; ++rd) {
+    const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
+    const bool live = item < p.lin.count;
+    double2 v[Cfg::E];
+    if (live) {
+      const long long ib = p.lin.base(item), ies = p.lin.es;
+      const double2* F = (const double2*)p.F;
+      sfor<CL>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+          sfor<RL>([&](auto Ki) HC_INL {
+            const long long kp = beta + (long long)RpL * Ki;
+            v[c * RL + Ki] = F[ib + (p.ref_order ? ref_index(a, kp) : kp) * ies];
+          });
+      });
+    }
+    fft_inverse<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X, mt, tid, sync, p0);
+    if (!live) continue;
+    const long long ob = p.lout.base(item);
+    const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
+    store_pass0<SYM, Cfg>(v, a, tb, em, p.v, tid);
+  }
+}
+
 // ---------------------------------------------------------------- pfft fwd --
 template <int SYM, class Cfg, int G>
 __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {

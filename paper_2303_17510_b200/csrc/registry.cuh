@@ -22,7 +22,22 @@ struct KernelEntry {
   int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
   int xs = 0, stash = 0;           // exchange buffer / shared-memory stash per group (complex)
   bool pair = false;               // conv kernel is k_conv1d_pair (two exchange buffers per group)
+  // column-tile outer-axis passes (complex / centered only): GC interleaved column groups
+  int gc = 0;
+  const void* fwdc_fn = nullptr;
+  const void* bwdc_fn = nullptr;
+  void (*fwdc)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  void (*bwdc)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
 };
+
+// column groups per CTA: up to 8 adjacent columns (128 B rows), <= 1024 threads, and the
+// interleaved exchange buffers within ~200 KB of shared memory
+template <class Cfg>
+constexpr int column_groups() {
+  int g = 8;
+  while (g > 1 && (g * Cfg::T > 1024 || (long long)g * Cfg::XS * 16 > 200 * 1024)) g /= 2;
+  return g;
+}
 
 // SMEM_STASH: keep the first spectrum in shared memory even when it would fit in registers
 // (lets G > 1 line groups share an SM within the register budget).
@@ -59,6 +74,18 @@ KernelEntry make_entry(const char* radix) {
   e.bwd = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
     k_pfft_bwd<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
   };
+  if constexpr (SYM != SYM_HERMITIAN) {
+    constexpr int GC = column_groups<Cfg>();
+    e.gc = GC;
+    e.fwdc_fn = (const void*)k_pfft_fwd_cols<SYM, Cfg, GC>;
+    e.bwdc_fn = (const void*)k_pfft_bwd_cols<SYM, Cfg, GC>;
+    e.fwdc = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+      k_pfft_fwd_cols<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+    };
+    e.bwdc = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+      k_pfft_bwd_cols<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+    };
+  }
   return e;
 }
 
