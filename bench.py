@@ -194,7 +194,7 @@ def run_reference(args):
         return
     name = args.config
     dims, axes, C_, shape, n_out = config_sizes(name)
-    arm = CpuArm(name, args.m)
+    arm = CpuArm(name, int(str(args.m).split(",")[0]) if args.m else None)
     arm.size_for(max(0.5, 120.0 / (args.steps + args.warmup)))  # whole run ~2 minutes
     vals, dts = [], []
     for i in range(args.warmup + args.steps):
@@ -234,13 +234,18 @@ def run_cuda(args):
     dims, axes, C_, shape, n_out = config_sizes(name)
     stream = torch.cuda.current_stream()
 
-    # plan (planner runs here, outside the timed region)
+    # plan (planner runs here, outside the timed region); --m: one size for every axis or a list
+    ms = [None] * dims
+    if args.m:
+        vals = [int(x) for x in str(args.m).split(",")]
+        ms = vals if len(vals) == dims else [vals[0]] * dims
     if dims == 1:
         L, M, s = axes[0]
-        plan = hconv.Conv1dPlan(L, M, args.m, hconv.Symmetry(s), C_=C_, device=local)
+        plan = hconv.Conv1dPlan(L, M, ms[0], hconv.Symmetry(s), C_=C_, device=local)
         params = [plan.params]
     else:
-        plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, args.m, hconv.Symmetry(s)) for (L, M, s) in axes], device=local)
+        plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, mk, hconv.Symmetry(s)) for (L, M, s), mk in zip(axes, ms)],
+                                device=local)
         params = plan.params
     full_shape = (C_, *shape) if dims == 1 else tuple(shape)
     f = torch.empty(full_shape, dtype=torch.complex128, device=dev)
@@ -382,7 +387,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
-    ap.add_argument("--m", type=int, default=None, help="force the subtransform size (default: planner)")
+    ap.add_argument("--m", default=None, help="force subtransform size(s): one value or one per axis, comma separated")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -674,6 +674,145 @@ void check_desc(const hconv_desc* d) {
   if (d->A != 2 || d->B != 1) throw Unsupported("builtin product kernels are binary: A == 2, B == 1");
 }
 
+// Build the axis plans for chosen subtransform sizes and allocate the N-D work buffers.
+void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<hb::Symmetry>& syms) {
+  const hconv_desc* desc = &P->d;
+  const int d = desc->dims;
+  for (double2* b : P->buffers)
+    if (b) cudaFree(b);
+  P->buffers.clear();
+  P->ax.clear();
+  for (int k = 0; k < d; ++k) P->ax.push_back(make_axis(hb::deriveParams(desc->axis[k].L, desc->axis[k].M, ms[k], syms[k])));
+  if (d == 1) {
+    P->ax[0].pp.C = desc->C ? desc->C : 1;
+    return;
+  }
+  long long NB = 1;
+  for (int l = 0; l < d - 1; ++l) {
+    const long long inner = (long long)inner_elems(P, l);
+    const long long work = NB * P->ax[l].dev.B * inner, acc = NB * (long long)P->ax[l].data * inner;
+    for (size_t a = 0; a < desc->A; ++a) {
+      double2* b = nullptr;
+      CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
+      P->buffers.push_back(b);
+    }
+    double2* b = nullptr;
+    CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
+    P->buffers.push_back(b);
+    NB *= P->ax[l].dev.B;
+  }
+}
+
+// N-D planning (tune_nd).  Each axis is first tuned independently with 1D
+// convolutions; on the GPU the number of outer residue blocks multiplies
+// full passes over the volume, so the best per-axis candidates (top 2 by 1D time, plus the
+// fewest-residue candidate) are then timed together on the real N-D convolution.
+std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms, const std::vector<size_t>& data) {
+  const hconv_desc* desc = &P->d;
+  const int d = desc->dims;
+  std::string key = dev_info().name + "|nd";
+  for (int k = 0; k < d; ++k)
+    key += "|" + std::string(hb::name(syms[k])) + ":" + std::to_string(desc->axis[k].L) + ":" +
+           std::to_string(desc->axis[k].M) + ":" + std::to_string(desc->axis[k].m);
+  auto& cache = planner_cache();
+  {
+    std::lock_guard<std::mutex> lk(cache.mu);
+    cache.load();
+    auto it = cache.mem.find(key + "|axis0");
+    if (it != cache.mem.end()) {
+      std::vector<size_t> ms(d);
+      bool ok = true;
+      for (int k = 0; k < d; ++k) {
+        auto jt = cache.mem.find(key + "|axis" + std::to_string(k));
+        if (jt == cache.mem.end()) ok = false;
+        else ms[k] = jt->second.first;
+      }
+      if (ok) {
+        P->report.cached = true;
+        return ms;
+      }
+    }
+  }
+  std::vector<std::vector<size_t>> options(d);
+  for (int k = 0; k < d; ++k) {
+    const hconv_axis& a = desc->axis[k];
+    if (a.m) {
+      options[k] = {a.m};
+      continue;
+    }
+    long long lines = 1;
+    for (int j = 0; j < d; ++j)
+      if (j != k) lines *= (long long)data[j];
+    lines = std::min<long long>(lines, 2048);
+    PlanReport r;
+    const size_t best = tune_axis(syms[k], a.L, a.M, lines, &r);
+    options[k].push_back(best);
+    if (!r.timed.empty()) {
+      std::vector<Candidate> c = r.timed;
+      std::sort(c.begin(), c.end(), [](const Candidate& x, const Candidate& y) { return x.ms < y.ms; });
+      for (size_t i = 0; i < c.size() && options[k].size() < 2; ++i)
+        if (c[i].m != best) options[k].push_back(c[i].m);
+      const Candidate* fewest = &c[0];
+      for (const auto& x : c)
+        if (x.pp.n < fewest->pp.n || (x.pp.n == fewest->pp.n && x.ms < fewest->ms)) fewest = &x;
+      if (std::find(options[k].begin(), options[k].end(), fewest->m) == options[k].end()) options[k].push_back(fewest->m);
+    }
+    for (const auto& x : r.timed) P->report.timed.push_back(x);
+  }
+  size_t total = 1;
+  for (auto& o : options) total *= o.size();
+  std::vector<size_t> best(d);
+  for (int k = 0; k < d; ++k) best[k] = options[k][0];
+  if (total > 1) {
+    size_t elems = 1;
+    for (size_t x : data) elems *= x;
+    double2 *f = nullptr, *g = nullptr, *o = nullptr;
+    CK(cudaMalloc(&f, elems * sizeof(double2)));
+    CK(cudaMalloc(&g, elems * sizeof(double2)));
+    CK(cudaMalloc(&o, elems * sizeof(double2)));
+    k_fill_uniform<<<256, 256>>>(7, 0, 0, (long long)elems, f);
+    k_fill_uniform<<<256, 256>>>(7, 1, 0, (long long)elems, g);
+    CK(cudaGetLastError());
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double best_ms = 1e30;
+    std::vector<size_t> ms(d);
+    for (size_t c = 0; c < total; ++c) {
+      size_t rem = c;
+      for (int k = d - 1; k >= 0; --k) {
+        ms[k] = options[k][rem % options[k].size()];
+        rem /= options[k].size();
+      }
+      build_plan(P, ms, syms);
+      const double2* ins[2] = {f, g};
+      nd_level(P, 0, 1, ins, o, 0);
+      double t = 1e30;
+      for (int r = 0; r < 2; ++r) {
+        CK(cudaEventRecord(e0));
+        nd_level(P, 0, 1, ins, o, 0);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float x = 0;
+        CK(cudaEventElapsedTime(&x, e0, e1));
+        t = std::min<double>(t, x);
+      }
+      if (t < best_ms * (1 - 1e-9)) {
+        best_ms = t;
+        best = ms;
+      }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(f);
+    cudaFree(g);
+    cudaFree(o);
+  }
+  std::lock_guard<std::mutex> lk(cache.mu);
+  for (int k = 0; k < d; ++k) cache.store(key + "|axis" + std::to_string(k), best[k], 0.0);
+  return best;
+}
+
 }  // namespace
 
 extern "C" {
@@ -779,47 +918,26 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
     P->device = desc->device;
     const int d = desc->dims;
     const bool herm = desc->axis[d - 1].symmetry == HCONV_HERMITIAN;
-    // data extents first (needed for per-axis tuning batch sizes)
-    std::vector<size_t> data(d);
+    std::vector<size_t> data(d), ms(d);
     std::vector<hb::Symmetry> syms(d);
+    bool tune = false;
     for (int k = 0; k < d; ++k) {
       int s = desc->axis[k].symmetry;
       if (herm && k < d - 1) s = HCONV_CENTERED;  // outer axes of a Hermitian convolution
       syms[k] = to_sym(s);
       data[k] = hb::deriveParams(desc->axis[k].L, desc->axis[k].M, 1, syms[k]).dataLength();
+      ms[k] = desc->axis[k].m;
+      tune |= ms[k] == 0;
     }
-    for (int k = 0; k < d; ++k) {
-      const hconv_axis& a = desc->axis[k];
-      size_t m = a.m;
-      if (m == 0) {
-        long long lines = 1;
-        if (d == 1) lines = (long long)(desc->C ? desc->C : 1);
-        else
-          for (int j = 0; j < d; ++j)
-            if (j != k) lines *= (long long)data[j];
-        lines = std::min<long long>(lines, 2048);
-        m = tune_axis(syms[k], a.L, a.M, lines, &P->report);
-      }
-      P->ax.push_back(make_axis(hb::deriveParams(a.L, a.M, m, syms[k])));
-    }
-    if (d == 1) {
-      P->ax[0].pp.C = desc->C ? desc->C : 1;
-    } else {
-      long long NB = 1;
-      for (int l = 0; l < d - 1; ++l) {
-        const long long inner = (long long)inner_elems(P.get(), l);
-        const long long work = NB * P->ax[l].dev.B * inner, acc = NB * (long long)P->ax[l].data * inner;
-        for (size_t a = 0; a < desc->A; ++a) {
-          double2* b = nullptr;
-          CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
-          P->buffers.push_back(b);
-        }
-        double2* b = nullptr;
-        CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
-        P->buffers.push_back(b);
-        NB *= P->ax[l].dev.B;
+    if (tune) {
+      if (d == 1) {
+        const long long lines = std::min<long long>((long long)(desc->C ? desc->C : 1), 2048);
+        ms[0] = tune_axis(syms[0], desc->axis[0].L, desc->axis[0].M, lines, &P->report);
+      } else {
+        ms = tune_nd(P.get(), syms, data);
       }
     }
+    build_plan(P.get(), ms, syms);
     *out = P.release();
   });
 }
