@@ -47,6 +47,7 @@ struct AxisDev {
   int ns1, nu, nc;      // Ns1, rows of U (2 R0 + 1), rows of Cv
   int oMT, oU, oC, oA, oZ, oH, oBl, oBh;
   int tabn;             // entries staged in shared memory (>= the middle-pass tables)
+  int tabfull;          // entries the kernel reads (all staged when tabn >= tabfull)
 };
 
 // ---- table accessors (radix kernels) ----
@@ -58,11 +59,10 @@ struct AxisDev {
 //  Bl[b]    = zeta_B^b, Bh[a] = zeta_B^{Ns1 a}   (Hermitian packing)
 //  MT       = middle-pass twiddles (FFTCfg::MT layout)
 // order in memory: MT U C A Z H Bl Bh -- the kernel stages the longest prefix that fits
-// The first a.tabn entries are staged into shared memory at kernel start (tb); the rest, when
-// the shared-memory budget is exhausted, are read through the read-only cache.
-__device__ __forceinline__ double2 tget(const AxisDev& a, const double2* tb, int i) {
-  return i < a.tabn ? tb[i] : __ldg(a.tab + i);
-}
+// tb: the tables as the kernel reads them -- the shared-memory copy when everything was
+// staged (a.tabn >= a.tabfull), else the global copy (the middle-pass tables MT are always
+// read from shared memory, see kernels.cuh).
+__device__ __forceinline__ double2 tget(const AxisDev& a, const double2* tb, int i) { return tb[i]; }
 __device__ __forceinline__ double2 tA(const AxisDev& a, const double2* tb, int b) { return tget(a, tb, a.oA + b); }
 __device__ __forceinline__ double2 tZ(const AxisDev& a, const double2* tb, int v, int b) { return tget(a, tb, a.oZ + v * a.ns1 + b); }
 __device__ __forceinline__ double2 tU(const AxisDev& a, const double2* tb, int v, int i) { return tget(a, tb, a.oU + v * a.nu + i); }

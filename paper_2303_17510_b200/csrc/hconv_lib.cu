@@ -213,6 +213,7 @@ void build_tables(AxisPlan& ap) {
   a.oBh = a.oBl + ns1;
   ap.tab_full = a.sym == hc::SYM_HERMITIAN ? a.oBh + R0 + 1 : a.oH;
   a.tabn = ap.tab_full;
+  a.tabfull = ap.tab_full;
   const int total = a.oBh + R0 + 1;
   auto key = std::make_tuple((int)a.Bc, a.qm, a.B, a.n, nc, (const void*)k);
   int d = 0;

@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
   const int stage = p.stage;
   const bool stage_acc = stage != 0 && !STASH_REGS && a.S <= Cfg::N;
   if (stage && tid == 0) {
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       const double2* fnext = !last ? p.f + base : (item + step < p.lin.count ? p.f + p.lin.base(item + step) : nullptr);
       double2 v[Cfg::E];
       double2 Fr[STASH_REGS ? Cfg::E : 1];
-      const P0Res<SYM> p0{&a, tb, res};
+      const P0Res<SYM> p0{&a, tp, res};
       // ---- forward padded FFTs of the A = 2 inputs (one code copy: keeps the kernel inside
       //      the instruction cache); input 0 is stashed, input 1 multiplied by it
 #pragma unroll 1
@@ -177,11 +178,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
         if (stage) {
           mbar_wait(bar_in, ph_in);
           ph_in ^= 1;
-          load_pass0<SYM, Cfg>(v, a, tb, IN, 1, res, tid);
+          load_pass0<SYM, Cfg>(v, a, tp, IN, 1, res, tid);
           sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
           if (stage == 2 && tid == 0 && nxt) tma_copy(IN, nxt, row_bytes, bar_in);
         } else {
-          load_pass0<SYM, Cfg>(v, a, tb, src + base, es, res, tid);
+          load_pass0<SYM, Cfg>(v, a, tp, src + base, es, res, tid);
         }
         fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
           if (stage == 1 && inp == 0 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
@@ -232,10 +233,10 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
       }
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
-        store_herm<Cfg>(v, a, tb, em, res, tid, X, sync);
+        store_herm<Cfg>(v, a, tp, em, res, tid, X, sync);
         if (stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       } else {
-        store_pass0<SYM, Cfg>(v, a, tb, em, res, tid);
+        store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
       }
       if (stage_acc) sync();  // stash (acc) reads done before the next residue stashes F
     }
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
   const GroupSync sync{g + 1, Cfg::T};
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
   const bool stage = p.stage == 1;
   if (stage && tid == 0) {
     mbar_init(bar_f, 1);
@@ -284,18 +286,18 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
       const bool more = item + step < p.lin.count;
       const long long nbase = last ? (more ? p.lin.base(item + step) : -1) : base;
       double2 v[Cfg::E], w[Cfg::E];
-      const P0Res<SYM> p0{&a, tb, res};
+      const P0Res<SYM> p0{&a, tp, res};
       if (stage) {
         mbar_wait(bar_f, ph_f);
         ph_f ^= 1;
         mbar_wait(bar_g, ph_g);
         ph_g ^= 1;
-        load_pass0<SYM, Cfg>(v, a, tb, X, 1, res, tid);
-        load_pass0<SYM, Cfg>(w, a, tb, Y, 1, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
+        load_pass0<SYM, Cfg>(w, a, tp, Y, 1, res, tid);
         sync();
       } else {
-        load_pass0<SYM, Cfg>(v, a, tb, p.f + base, es, res, tid);
-        load_pass0<SYM, Cfg>(w, a, tb, p.g + base, es, res, tid);
+        load_pass0<SYM, Cfg>(v, a, tp, p.f + base, es, res, tid);
+        load_pass0<SYM, Cfg>(w, a, tp, p.g + base, es, res, tid);
       }
       fft_forward_pair<Cfg>(v, w, X, Y, mt, tid, sync, p0, [&]() HC_INL {
         if (stage && tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
@@ -317,10 +319,10 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
       const double2* acc = res > 0 ? slot : nullptr;
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
-        store_herm<Cfg>(v, a, tb, em, res, tid, X, sync);
+        store_herm<Cfg>(v, a, tp, em, res, tid, X, sync);
         if (stage && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
       } else {
-        store_pass0<SYM, Cfg>(v, a, tb, em, res, tid);
+        store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
       }
     }
   }
@@ -344,13 +346,14 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols(FwdArgs p) {
   const CtaSync sync;
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
-  const P0Res<SYM> p0{&a, tb, p.v};
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
   const long long rounds = (p.lin.count + (long long)gridDim.x * GC - 1) / ((long long)gridDim.x * GC);
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
     const bool live = item < p.lin.count;
     double2 v[Cfg::E];
-    if (live) load_pass0<SYM, Cfg>(v, a, tb, p.f + p.lin.base(item), p.lin.es, p.v, tid);
+    if (live) load_pass0<SYM, Cfg>(v, a, tp, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X, mt, tid, sync, p0);
     if (!live) continue;
     const long long ob = p.lout.base(item), oes = p.lout.es;
@@ -379,7 +382,8 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
   const CtaSync sync;
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
-  const P0Res<SYM> p0{&a, tb, p.v};
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
   const long long rounds = (p.lin.count + (long long)gridDim.x * GC - 1) / ((long long)gridDim.x * GC);
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
     if (!live) continue;
     const long long ob = p.lout.base(item);
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
-    store_pass0<SYM, Cfg>(v, a, tb, em, p.v, tid);
+    store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
   }
 }
 
@@ -418,10 +422,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
-  const P0Res<SYM> p0{&a, tb, p.v};
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
-    load_pass0<SYM, Cfg>(v, a, tb, p.f + p.lin.base(item), p.lin.es, p.v, tid);
+    load_pass0<SYM, Cfg>(v, a, tp, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item), oes = p.lout.es;
     sfor<CL>([&](auto Ci) HC_INL {
@@ -458,7 +463,8 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
-  const P0Res<SYM> p0{&a, tb, p.v};
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
   for (long long item = (long long)blockIdx.x * G + g; item < p.lin.count; item += (long long)gridDim.x * G) {
     double2 v[Cfg::E];
     const long long ib = p.lin.base(item), ies = p.lin.es;
@@ -482,8 +488,8 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_bwd(BwdArgs p) {
     fft_inverse<Cfg>(v, X, mt, tid, sync, p0);
     const long long ob = p.lout.base(item);
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
-    if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, tb, em, p.v, tid, X, sync);
-    else store_pass0<SYM, Cfg>(v, a, tb, em, p.v, tid);
+    if constexpr (SYM == SYM_HERMITIAN) store_herm<Cfg>(v, a, tp, em, p.v, tid, X, sync);
+    else store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
   }
 }
 
