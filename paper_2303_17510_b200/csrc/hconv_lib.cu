@@ -616,7 +616,7 @@ struct hconv_plan {
   std::vector<AxisPlan> ax;
   Scratch scratch;                    // conv1d accumulator slots
   std::vector<double2*> buffers;      // N-D work / accumulator buffers
-  std::vector<size_t> level_work, level_acc;  // per level: elements of one work buffer / acc
+  std::vector<long long> chunk;               // per level: arrays processed per pass (L2 blocking)
   PlanReport report;
   ~hconv_plan() {
     scratch.release();
@@ -651,20 +651,29 @@ void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, 
     launch_conv(ap, lin, in[0], in[1], out, P->scratch, s);
     return;
   }
-  const long long B = ap.dev.B, n = ap.dev.n;
-  const hc::Lines cols{NB * inner, inner, asz, 1, inner};       // columns of the input arrays
-  const hc::Lines wcols{NB * inner, inner, B * inner, 1, inner};  // columns of the work arrays
-  double2* acc = level_acc(P, level);
-  std::vector<const double2*> sub(P->d.A);
-  for (size_t a = 0; a < P->d.A; ++a) sub[a] = level_work(P, level, (int)a);
-  const double scale = 1.0 / (double)ap.dev.qm;
-  for (int v = 0; v < n; ++v) {
-    for (size_t a = 0; a < P->d.A; ++a) launch_fwd(ap, cols, wcols, in[a], level_work(P, level, (int)a), v, 0, s);
-    nd_level(P, level + 1, NB * B, sub.data(), level_work(P, level, 0), s);
-    const bool first = v == 0, last = v == n - 1;
-    double2* dst = last ? out : acc;
-    const double2* accsrc = first ? nullptr : acc;
-    launch_bwd(ap, wcols, cols, level_work(P, level, 0), dst, accsrc, last ? scale : 1.0, v, 0, s);
+  // L2 blocking: below the top level the NB arrays (spectral planes of the parent axis) are
+  // processed `chunk` at a time, so this level's work buffers are reused while L2-resident
+  const long long chunk = std::max<long long>(1, P->chunk[level]);
+  for (long long c0 = 0; c0 < NB; c0 += chunk) {
+    const long long nb = std::min(chunk, NB - c0);
+    std::vector<const double2*> inc(P->d.A);
+    for (size_t a = 0; a < P->d.A; ++a) inc[a] = in[a] + c0 * asz;
+    double2* outc = out + c0 * asz;
+    const long long B = ap.dev.B, n = ap.dev.n;
+    const hc::Lines cols{nb * inner, inner, asz, 1, inner};       // columns of the input arrays
+    const hc::Lines wcols{nb * inner, inner, B * inner, 1, inner};  // columns of the work arrays
+    double2* acc = level_acc(P, level);
+    std::vector<const double2*> sub(P->d.A);
+    for (size_t a = 0; a < P->d.A; ++a) sub[a] = level_work(P, level, (int)a);
+    const double scale = 1.0 / (double)ap.dev.qm;
+    for (int v = 0; v < n; ++v) {
+      for (size_t a = 0; a < P->d.A; ++a) launch_fwd(ap, cols, wcols, inc[a], level_work(P, level, (int)a), v, 0, s);
+      nd_level(P, level + 1, nb * B, sub.data(), level_work(P, level, 0), s);
+      const bool first = v == 0, last = v == n - 1;
+      double2* dst = last ? outc : acc;
+      const double2* accsrc = first ? nullptr : acc;
+      launch_bwd(ap, wcols, cols, level_work(P, level, 0), dst, accsrc, last ? scale : 1.0, v, 0, s);
+    }
   }
 }
 
@@ -688,10 +697,18 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
     P->ax[0].pp.C = desc->C ? desc->C : 1;
     return;
   }
+  // level l processes `chunk[l]` arrays per pass: all of them at the top level, and below it
+  // as many as keep this level's buffers within HCONV_ND_BLOCK_MB (default 96 MB, L2-resident)
+  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 96.0;
+  P->chunk.assign(d, 1);
   long long NB = 1;
   for (int l = 0; l < d - 1; ++l) {
     const long long inner = (long long)inner_elems(P, l);
-    const long long work = NB * P->ax[l].dev.B * inner, acc = NB * (long long)P->ax[l].data * inner;
+    const long long per = (long long)(desc->A * P->ax[l].dev.B + P->ax[l].data) * inner * (long long)sizeof(double2);
+    long long ch = NB;
+    if (l > 0 && block_mb > 0) ch = std::max<long long>(1, std::min<long long>(NB, (long long)(block_mb * 1048576.0 / per)));
+    P->chunk[l] = ch;
+    const long long work = ch * P->ax[l].dev.B * inner, acc = ch * (long long)P->ax[l].data * inner;
     for (size_t a = 0; a < desc->A; ++a) {
       double2* b = nullptr;
       CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
@@ -700,7 +717,7 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
     double2* b = nullptr;
     CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
     P->buffers.push_back(b);
-    NB *= P->ax[l].dev.B;
+    NB = ch * P->ax[l].dev.B;
   }
 }
 
@@ -953,15 +970,11 @@ hconv_status hconv_plan_params(const hconv_plan* p, int axis, hconv_params* o) {
 size_t hconv_plan_workspace_bytes(const hconv_plan* p) {
   if (!p) return 0;
   size_t b = p->scratch.bytes;
-  if (p->d.dims > 1) {
-    long long NB = 1;
-    const int d = p->d.dims;
-    for (int l = 0; l < d - 1; ++l) {
-      size_t inner = 1;
-      for (int k = l + 1; k < d; ++k) inner *= p->ax[k].data;
-      b += (size_t)NB * (p->ax[l].dev.B * p->d.A + p->ax[l].data) * inner * sizeof(double2);
-      NB *= p->ax[l].dev.B;
-    }
+  const int d = p->d.dims;
+  for (int l = 0; l + 1 < d; ++l) {
+    size_t inner = 1;
+    for (int k = l + 1; k < d; ++k) inner *= p->ax[k].data;
+    b += (size_t)p->chunk[l] * (p->ax[l].dev.B * p->d.A + p->ax[l].data) * inner * sizeof(double2);
   }
   return b;
 }
