@@ -128,8 +128,8 @@ __device__ __forceinline__ void stage_tables(double2* tb, const AxisDev& a, int 
 // accumulator are brought on chip by TMA bulk copies issued one phase ahead -- the next line
 // copy starts as soon as the previous transform has released the exchange buffer, so the
 // HBM/L2 latency overlaps the butterflies of the current transform.
-template <int SYM, class Cfg, int G, bool STASH_REGS>
-__global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d(ConvArgs p) {
+template <int SYM, class Cfg, int G, bool STASH_REGS, int MINB = 1>
+__global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
   extern __shared__ __align__(16) double2 smem[];
   __shared__ __align__(8) uint64_t bars[2 * G];
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);

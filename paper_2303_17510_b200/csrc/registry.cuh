@@ -41,7 +41,8 @@ constexpr int column_groups() {
 
 // SMEM_STASH: keep the first spectrum in shared memory even when it would fit in registers
 // (lets G > 1 line groups share an SM within the register budget).
-template <int SYM, class Cfg, int G, bool SMEM_STASH = false>
+// MINB: minimum resident CTAs per SM requested from ptxas (caps registers per thread)
+template <int SYM, class Cfg, int G, bool SMEM_STASH = false, int MINB = 1>
 KernelEntry make_entry(const char* radix) {
   constexpr bool SR = Cfg::E <= 16 && !SMEM_STASH;
   // paired forward FFTs (k_conv1d_pair) measured slower than the stash path on B200 (r01:
@@ -61,12 +62,12 @@ KernelEntry make_entry(const char* radix) {
   e.stash = PAIR ? Cfg::XS : (SR ? 0 : Cfg::N);  // pair: the second exchange buffer Y
   e.pair = PAIR;
   if constexpr (PAIR) e.conv_fn = (const void*)k_conv1d_pair<SYM, Cfg, G>;
-  else e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR>;
+  else e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR, MINB>;
   e.fwd_fn = (const void*)k_pfft_fwd<SYM, Cfg, G>;
   e.bwd_fn = (const void*)k_pfft_bwd<SYM, Cfg, G>;
   e.conv = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
     if constexpr (PAIR) k_conv1d_pair<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
-    else k_conv1d<SYM, Cfg, G, SR><<<grid, Cfg::T * G, sm, s>>>(a);
+    else k_conv1d<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
   };
   e.fwd = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
     k_pfft_fwd<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
@@ -113,14 +114,14 @@ KernelEntry make_naive_entry() {
 template <int SYM>
 inline void build_registry(KernelEntry* out, int* count) {
   int k = 0;
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4>("8x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4>("16x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4>("4x8x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, 2>("8x8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4, false, 4>("8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4, false, 4>("16x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, 2, false, 4>("8x8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, 2>("16x16x4");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1>("16x16x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1, true, 3>("16x16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1>("16x16x16");
   // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
