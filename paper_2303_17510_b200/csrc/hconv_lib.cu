@@ -544,6 +544,12 @@ struct PlanReport {
   bool cached = false;
 };
 
+// timed candidate lists of this process, by planner key (a cache hit still knows the ranking)
+std::map<std::string, std::vector<Candidate>>& ranked_memo() {
+  static std::map<std::string, std::vector<Candidate>> m;
+  return m;
+}
+
 // tune_1d on the device: median of 5 timed runs after one warm-up, CUDA events.
 size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanReport* rep) {
   auto& cache = planner_cache();
@@ -553,7 +559,11 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
     cache.load();
     auto it = cache.mem.find(key);
     if (it != cache.mem.end()) {
-      if (rep) rep->cached = true;
+      if (rep) {
+        rep->cached = true;
+        auto jt = ranked_memo().find(key);
+        if (jt != ranked_memo().end()) rep->timed = jt->second;
+      }
       return it->second.first;
     }
   }
@@ -603,6 +613,7 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
   cudaFree(o);
   if (rep) rep->timed = cands;
   std::lock_guard<std::mutex> lk(cache.mu);
+  ranked_memo()[key] = cands;
   cache.store(key, best, best_ms);
   return best;
 }
@@ -775,6 +786,15 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
         if (x.pp.n < fewest->pp.n || (x.pp.n == fewest->pp.n && x.ms < fewest->ms)) fewest = &x;
       if (std::find(options[k].begin(), options[k].end(), fewest->m) == options[k].end()) options[k].push_back(fewest->m);
     }
+    if (r.timed.empty()) {  // planner cache from an earlier process: add the fewest-residue class
+      auto c = plan_candidates(syms[k], a.L, a.M);
+      if (!c.empty()) {
+        const Candidate* fewest = &c[0];
+        for (const auto& x : c)
+          if (x.pp.n < fewest->pp.n) fewest = &x;
+        if (fewest->m != best) options[k].push_back(fewest->m);
+      }
+    }
     for (const auto& x : r.timed) P->report.timed.push_back(x);
   }
   size_t total = 1;
@@ -806,7 +826,7 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
       const double2* ins[2] = {f, g};
       nd_level(P, 0, 1, ins, o, 0);
       double t = 1e30;
-      for (int r = 0; r < 2; ++r) {
+      for (int r = 0; r < 3; ++r) {
         CK(cudaEventRecord(e0));
         nd_level(P, 0, 1, ins, o, 0);
         CK(cudaEventRecord(e1));
@@ -814,6 +834,11 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
         float x = 0;
         CK(cudaEventElapsedTime(&x, e0, e1));
         t = std::min<double>(t, x);
+      }
+      if (std::getenv("HCONV_PLAN_VERBOSE")) {
+        std::fprintf(stderr, "[hconv tune_nd]");
+        for (int k = 0; k < d; ++k) std::fprintf(stderr, " m%d=%zu", k, ms[k]);
+        std::fprintf(stderr, " %.3f ms\n", t);
       }
       if (t < best_ms * (1 - 1e-9)) {
         best_ms = t;
