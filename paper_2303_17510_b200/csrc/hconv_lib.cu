@@ -347,6 +347,15 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
   static const bool off = std::getenv("HCONV_NO_STAGE") && std::getenv("HCONV_NO_STAGE")[0] == '1';
   const int S = ap.dev.S;
   c.gs = k->xs + k->stash;
+  static const bool no_pp = std::getenv("HCONV_NO_PP") && std::getenv("HCONV_NO_PP")[0] == '1';
+  if (!off && !no_pp && !k->pair && lin.es == 1 && S <= k->xs &&
+      (size_t)(k->mt + (size_t)k->G * 2 * k->xs) * sizeof(double2) <= kSmemCap) {
+    c.stage = 3;  // ping-pong: X (f, its exchanges, stashed F) and Y (g, its and the inverse's exchanges)
+    c.gs = 2 * k->xs;
+    c.tabn = staged_tabn(ap, c.gs);
+    c.smem = (size_t)(c.tabn + (size_t)k->G * c.gs) * sizeof(double2);
+    return c;
+  }
   if (!off && lin.es == 1) {
     if (S <= k->xs) {
       c.stage = 1;
@@ -368,12 +377,34 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
                  Scratch& scratch, cudaStream_t s) {
   if (lin.count == 0) return;
   const ConvLayout cl = conv_layout(ap, lin);
-  const int grid = grid_for(ap.k->conv_fn, ap.k, cl.smem, lin.count);
+  const void* fn = cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
+  const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
-  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off};
+  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr};
+  // HCONV_DEBUG_SAME_LINE=1: every line reads/writes line 0 (L2-resident timing of the kernel
+  // body without HBM; diagnostics only, results are meaningless)
+  static const bool same = std::getenv("HCONV_DEBUG_SAME_LINE") && std::getenv("HCONV_DEBUG_SAME_LINE")[0] == '1';
+  if (same) a.lin.d_out = 0;
   a.ax.tabn = cl.tabn;
-  ap.k->conv(a, grid, cl.smem, s);
+  // HCONV_TRACE=1: phase timestamps (clock64) of CTA 0, printed to stderr (diagnostics)
+  static const bool trace = std::getenv("HCONV_TRACE") && std::getenv("HCONV_TRACE")[0] == '1';
+  unsigned long long* tbuf = nullptr;
+  if (trace && !ap.k->naive) {
+    CK(cudaMalloc(&tbuf, 256 * sizeof(unsigned long long)));
+    CK(cudaMemset(tbuf, 0, 256 * sizeof(unsigned long long)));
+    a.trace = tbuf;
+  }
+  if (cl.stage == 3) ap.k->convpp(a, grid, cl.smem, s);
+  else ap.k->conv(a, grid, cl.smem, s);
   CK(cudaGetLastError());
+  if (tbuf) {
+    unsigned long long h[256];
+    CK(cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost));
+    std::fprintf(stderr, "[hconv trace %s grid %d]", ap.k->radix, grid);
+    for (int i = 1; i < 256 && h[i]; ++i) std::fprintf(stderr, " %llu", h[i] - h[i - 1]);
+    std::fprintf(stderr, "\n");
+    cudaFree(tbuf);
+  }
 }
 
 // Column-tile variants for strided outer-axis lines (complex / centered radix kernels).

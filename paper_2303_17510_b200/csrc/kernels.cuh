@@ -24,6 +24,8 @@ struct ConvArgs {
   int stage;             // 0: pass-0 reads global; 1: lines staged by TMA into X; 2: into a separate buffer
   int gs;                // group stride in shared memory (complex)
   int in_off;            // stage 2: offset of the staging buffer inside the group region
+                         // stage 3: ping-pong kernel (k_conv1d_pp), X and Y of XS each
+  unsigned long long* trace;  // optional phase timestamps of CTA 0 / thread 0 (HCONV_TRACE)
 };
 
 struct FwdArgs {
@@ -159,9 +161,20 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
   double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
   long long item = (long long)blockIdx.x * G + g;
   if (stage && tid == 0 && item < p.lin.count) tma_copy(IN, p.f + p.lin.base(item), row_bytes, bar_in);
+  const bool tr = p.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  int tn = 0;
+  // trace points are preceded by a group barrier (when tracing) so they mark phase boundaries
+#define HC_TRACE()                                   \
+  do {                                               \
+    if (p.trace) {                                   \
+      sync();                                        \
+      if (tr && tn < 256) p.trace[tn++] = clock64(); \
+    }                                                \
+  } while (0)
   for (; item < p.lin.count; item += step) {
     const long long base = p.lin.base(item);
     for (int res = 0; res < a.n; ++res) {
+      HC_TRACE();
       const bool last = res == a.n - 1;
       // next f line: the same line for the next residue, else the next item's line
       const double2* fnext = !last ? p.f + base : (item + step < p.lin.count ? p.f + p.lin.base(item + step) : nullptr);
@@ -178,15 +191,18 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
         if (stage) {
           mbar_wait(bar_in, ph_in);
           ph_in ^= 1;
+          HC_TRACE();
           load_pass0<SYM, Cfg>(v, a, tp, IN, 1, res, tid);
           sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
           if (stage == 2 && tid == 0 && nxt) tma_copy(IN, nxt, row_bytes, bar_in);
         } else {
           load_pass0<SYM, Cfg>(v, a, tp, src + base, es, res, tid);
         }
+        HC_TRACE();
         fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
           if (stage == 1 && inp == 0 && tid == 0) tma_copy(IN, p.g + base, row_bytes, bar_in);
         });
+        HC_TRACE();
         if (inp == 0) {
           sfor<CL>([&](auto Ci) HC_INL {
             constexpr int c = Ci;
@@ -211,6 +227,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
           });
         }
       }
+      HC_TRACE();
       // ---- residue accumulator -> stash (its last reader was the product above)
       if (stage_acc && res > 0) {
         sync();
@@ -218,9 +235,11 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       }
       // ---- inverse; the next f copy into X starts once X is released (not for the
       //      Hermitian store, which uses X as its Z buffer)
+      HC_TRACE();
       fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
         if (SYM != SYM_HERMITIAN && stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       });
+      HC_TRACE();
       const double2* acc = nullptr;
       if (res > 0) {
         if (stage_acc) {
@@ -238,7 +257,109 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       } else {
         store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
       }
+      HC_TRACE();
       if (stage_acc) sync();  // stash (acc) reads done before the next residue stashes F
+    }
+  }
+#undef HC_TRACE
+}
+
+// --------------------------------------------------------- conv1d, ping-pong --
+// Two line buffers X and Y per group.  X stages f and then serves f's exchanges (and holds the
+// stashed spectrum F), Y stages g and then serves g's and the inverse's exchanges.  The copy of
+// the next f line into X starts as soon as F has been consumed by the product, the next g line
+// into Y as soon as the inverse releases Y: each copy gets a full transform of lead time.
+// Requires unit-stride lines of at most XS values (host: conv_layout).
+template <int SYM, class Cfg, int G, bool STASH_REGS, int MINB = 1>
+__global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2 * G];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
+  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  double2* tb = smem;
+  const double2* mt = tb;
+  double2* X = smem + p.ax.tabn + g * p.gs;
+  double2* Y = X + Cfg::XS;
+  uint64_t* bar_f = &bars[2 * g];
+  uint64_t* bar_g = &bars[2 * g + 1];
+  const GroupSync sync{g + 1, T};
+  const AxisDev& a = p.ax;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  if (tid == 0) {
+    mbar_init(bar_f, 1);
+    mbar_init(bar_g, 1);
+    fence_mbar_init();
+  }
+  sync();
+  uint32_t ph_f = 0, ph_g = 0;
+  const uint32_t row_bytes = (uint32_t)a.S * 16u;
+  const long long es = p.lin.es, step = (long long)gridDim.x * G;
+  double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
+  long long item = (long long)blockIdx.x * G + g;
+  if (tid == 0 && item < p.lin.count) {
+    tma_copy(X, p.f + p.lin.base(item), row_bytes, bar_f);
+    tma_copy(Y, p.g + p.lin.base(item), row_bytes, bar_g);
+  }
+  for (; item < p.lin.count; item += step) {
+    const long long base = p.lin.base(item);
+    for (int res = 0; res < a.n; ++res) {
+      const bool last = res == a.n - 1;
+      const long long nbase = !last ? base : (item + step < p.lin.count ? p.lin.base(item + step) : -1);
+      double2 v[Cfg::E];
+      double2 Fr[STASH_REGS ? Cfg::E : 1];
+      const P0Res<SYM> p0{&a, tp, res};
+      // ---- forward f (staged in X, exchanges in X)
+      mbar_wait(bar_f, ph_f);
+      ph_f ^= 1;
+      load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
+      sync();
+      fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
+        // F kept in registers: X is free right away for the next f line
+        if (STASH_REGS && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
+      });
+      sfor<CL>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+          sfor<RL>([&](auto Ki) HC_INL {
+            if constexpr (STASH_REGS) Fr[c * RL + Ki] = v[c * RL + Ki];
+            else X[Ki * NBL + tid + c * T] = v[c * RL + Ki];
+          });
+      });
+      // ---- forward g (staged in Y, exchanges in Y)
+      mbar_wait(bar_g, ph_g);
+      ph_g ^= 1;
+      load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
+      sync();
+      fft_forward<Cfg>(v, Y, mt, tid, sync, p0);
+      sfor<CL>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+          sfor<RL>([&](auto Ki) HC_INL {
+            double2 F;
+            if constexpr (STASH_REGS) F = Fr[c * RL + Ki];
+            else F = X[Ki * NBL + tid + c * T];
+            double2& G_ = v[c * RL + Ki];
+            if constexpr (SYM == SYM_HERMITIAN) G_ = make_double2(G_.x * F.x, G_.y * F.y);
+            else G_ = cmul(G_, F);
+          });
+      });
+      if constexpr (!STASH_REGS) {
+        sync();  // every thread has read its stashed F: X is free for the next f line
+        if (tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
+      }
+      // ---- inverse (exchanges in Y); the next g line goes to Y once Y is released
+      fft_inverse<Cfg>(v, Y, mt, tid, sync, p0, [&]() HC_INL {
+        if (SYM != SYM_HERMITIAN && tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+      });
+      const double2* acc = res > 0 ? slot : nullptr;
+      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
+      if constexpr (SYM == SYM_HERMITIAN) {
+        store_herm<Cfg>(v, a, tp, em, res, tid, Y, sync);
+        if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+      } else {
+        store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
+      }
     }
   }
 }

@@ -22,6 +22,8 @@ struct KernelEntry {
   int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
   int xs = 0, stash = 0;           // exchange buffer / shared-memory stash per group (complex)
   bool pair = false;               // conv kernel is k_conv1d_pair (two exchange buffers per group)
+  const void* convpp_fn = nullptr;  // ping-pong variant (k_conv1d_pp)
+  void (*convpp)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   // column-tile outer-axis passes (complex / centered only): GC interleaved column groups
   int gc = 0;
   const void* fwdc_fn = nullptr;
@@ -68,6 +70,10 @@ KernelEntry make_entry(const char* radix) {
   e.conv = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
     if constexpr (PAIR) k_conv1d_pair<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
     else k_conv1d<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
+  };
+  e.convpp_fn = (const void*)k_conv1d_pp<SYM, Cfg, G, SR, MINB>;
+  e.convpp = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
+    k_conv1d_pp<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
   };
   e.fwd = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
     k_pfft_fwd<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);

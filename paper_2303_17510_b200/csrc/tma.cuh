@@ -60,4 +60,14 @@ __device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t by
   }
 }
 
+// Warm L2 with a line that will be staged later (no shared-memory destination, no barrier).
+__device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
+  constexpr uint32_t kChunk = 32768;
+  for (uint32_t off = 0; off < bytes; off += kChunk) {
+    const uint32_t n = bytes - off < kChunk ? bytes - off : kChunk;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(static_cast<const char*>(src) + off), "r"(n)
+                 : "memory");
+  }
+}
+
 }  // namespace hc
