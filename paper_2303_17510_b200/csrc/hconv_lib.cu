@@ -380,7 +380,9 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   const void* fn = cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
   const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
-  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr};
+  hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr, 0};
+  static const int dbg = std::getenv("HCONV_DBG") ? std::atoi(std::getenv("HCONV_DBG")) : 0;
+  a.dbg = dbg;
   // HCONV_DEBUG_SAME_LINE=1: every line reads/writes line 0 (L2-resident timing of the kernel
   // body without HBM; diagnostics only, results are meaningless)
   static const bool same = std::getenv("HCONV_DEBUG_SAME_LINE") && std::getenv("HCONV_DEBUG_SAME_LINE")[0] == '1';

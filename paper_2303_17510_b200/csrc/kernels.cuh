@@ -26,6 +26,8 @@ struct ConvArgs {
   int in_off;            // stage 2: offset of the staging buffer inside the group region
                          // stage 3: ping-pong kernel (k_conv1d_pp), X and Y of XS each
   unsigned long long* trace;  // optional phase timestamps of CTA 0 / thread 0 (HCONV_TRACE)
+  int dbg;                    // diagnostics (HCONV_DBG bits, ping-pong kernel): 1 skip stores,
+                              // 2 skip pass-0 loads, 4 skip the product, 8 skip the inverse
 };
 
 struct FwdArgs {
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       // ---- forward f (staged in X, exchanges in X)
       mbar_wait(bar_f, ph_f);
       ph_f ^= 1;
-      load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
+      if (!(p.dbg & 2)) load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
       sync();
       fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
         // F kept in registers: X is free right away for the next f line
@@ -329,10 +331,10 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       // ---- forward g (staged in Y, exchanges in Y)
       mbar_wait(bar_g, ph_g);
       ph_g ^= 1;
-      load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
+      if (!(p.dbg & 2)) load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
       sync();
       fft_forward<Cfg>(v, Y, mt, tid, sync, p0);
-      sfor<CL>([&](auto Ci) HC_INL {
+      if (!(p.dbg & 4)) sfor<CL>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
           sfor<RL>([&](auto Ki) HC_INL {
@@ -348,17 +350,39 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
         sync();  // every thread has read its stashed F: X is free for the next f line
         if (tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
       }
-      // ---- inverse (exchanges in Y); the next g line goes to Y once Y is released
-      fft_inverse<Cfg>(v, Y, mt, tid, sync, p0, [&]() HC_INL {
-        if (SYM != SYM_HERMITIAN && tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
-      });
+      // ---- inverse (exchanges in Y).  Once Y is released it receives the accumulator slot
+      //      (after residue 0, so the stores' read-modify-write never waits on L2) and then,
+      //      after the stores, the next g line; at residue 0 the next g line directly.
+      const bool acc_y = SYM != SYM_HERMITIAN && res > 0;
+      auto release_y = [&]() HC_INL {
+        if (SYM != SYM_HERMITIAN && tid == 0) {
+          if (acc_y) tma_copy(Y, slot, row_bytes, bar_g);
+          else if (nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+        }
+      };
+      if (!(p.dbg & 8)) {
+        fft_inverse<Cfg>(v, Y, mt, tid, sync, p0, release_y);
+      } else {
+        sync();
+        release_y();
+      }
       const double2* acc = res > 0 ? slot : nullptr;
+      if (acc_y) {
+        mbar_wait(bar_g, ph_g);
+        ph_g ^= 1;
+        acc = Y;
+      }
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
         store_herm<Cfg>(v, a, tp, em, res, tid, Y, sync);
         if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
       } else {
-        store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
+        if (!(p.dbg & 1)) store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
+        else if (v[0].x == 12345.678) p.out[0] = v[1];  // keep the work alive
+        if (acc_y) {
+          sync();  // every thread has read its accumulator values from Y
+          if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+        }
       }
     }
   }
