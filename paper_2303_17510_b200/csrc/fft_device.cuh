@@ -77,7 +77,12 @@ __device__ __forceinline__ double2 twc(double2 x) {
   }
 }
 
+#ifndef HC_FF_MODE
+#define HC_FF_MODE 1
+#endif
 constexpr int first_factor(int R) {
+  if (HC_FF_MODE == 1 && R % 8 == 0 && R != 8 && R % 3 == 0) return 8;   // 24 = 8 x 3
+  if (HC_FF_MODE == 2 && R % 3 == 0 && R != 3) return 3;                 // 24 = 3 x 8, 12 = 3 x 4
   if (R % 4 == 0 && R != 4) return 4;
   for (int f : {2, 3, 5, 7}) if (R % f == 0 && R != f) return f;
   return R;  // prime

@@ -348,8 +348,9 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
   const int S = ap.dev.S;
   c.gs = k->xs + k->stash;
   static const bool no_pp = std::getenv("HCONV_NO_PP") && std::getenv("HCONV_NO_PP")[0] == '1';
+  // (the ping-pong kernel reads every table from shared memory: all of them must fit)
   if (!off && !no_pp && !k->pair && lin.es == 1 && S <= k->xs &&
-      (size_t)(k->mt + (size_t)k->G * 2 * k->xs) * sizeof(double2) <= kSmemCap) {
+      (size_t)(ap.tab_full + (size_t)k->G * 2 * k->xs) * sizeof(double2) <= kSmemCap) {
     c.stage = 3;  // ping-pong: X (f, its exchanges, stashed F) and Y (g, its and the inverse's exchanges)
     c.gs = 2 * k->xs;
     c.tabn = staged_tabn(ap, c.gs);

@@ -266,6 +266,123 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
 #undef HC_TRACE
 }
 
+// ------------------------------------------- ping-pong fast paths (complex / centered) --
+// The ping-pong kernel sees unit-stride lines staged in shared memory and (host:
+// conv_layout) every table staged in shared memory, so its pass-0 loads and post-processing
+// stores are written with int offsets into shared memory, table rows hoisted per residue, and
+// the fold terms (L > B only) in one uniform branch after the main loop instead of a loop per
+// element.  Same arithmetic as load_fast / store_fast (block_io.cuh).
+template <int SYM, class Cfg>
+__device__ __forceinline__ void load_pass0_pp(double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb,
+                                              const double2* X, int res, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
+  const int L = a.L, B = a.B;
+  const double2* Cv = tb + a.oC + res * a.nc;
+  if constexpr (SYM == SYM_COMPLEX) {
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int b = tid + c * Cfg::T;
+      if (bvalid<Cfg, 0>(c, tid))
+        sfor<R0>([&](auto Ai) HC_INL {
+          const int s = Ns1 * Ai + b;
+          v[c * R0 + Ai] = s < L ? X[s] : make_double2(0.0, 0.0);
+        });
+    });
+    if (L > B) {
+      sfor<C0>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int b = tid + c * Cfg::T;
+        if (bvalid<Cfg, 0>(c, tid))
+          sfor<R0>([&](auto Ai) HC_INL {
+            double2& x = v[c * R0 + Ai];
+            int t = 1;
+            for (int j = Ns1 * Ai + b + B; j < L; j += B, ++t) x = cadd(x, res ? cmul(X[j], Cv[t]) : X[j]);
+          });
+      });
+    }
+  } else {
+    const int H = a.H, LH = L - H, BH = B - H;
+    const double2 c1 = Cv[1];
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int b = tid + c * Cfg::T;
+      if (bvalid<Cfg, 0>(c, tid))
+        sfor<R0>([&](auto Ai) HC_INL {
+          const int s = Ns1 * Ai + b;
+          double2 x = s < LH ? X[s + H] : make_double2(0.0, 0.0);
+          if (s >= BH) x = cadd(x, res ? cmulc(X[s - BH], c1) : X[s - BH]);
+          v[c * R0 + Ai] = x;
+        });
+    });
+  }
+  if (res) {
+    const double2* U = tb + a.oU + res * a.nu;
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = cmul(v[c * R0 + Ai], U[Ai]); });
+    });
+  }
+}
+
+// dst[j] = (ACC ? acc[j] : 0) + w_j, times `scale` with streaming stores when FINAL; acc is the
+// residue accumulator staged in shared memory (unit stride), dst a unit-stride line.
+template <int SYM, class Cfg, bool ACC, bool FINAL>
+__device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb, double2* dst,
+                                               const double2* acc, double scale, int res, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
+  const int L = a.L, B = a.B;
+  const double2* Cv = tb + a.oC + res * a.nc;
+  auto put = [&](int j, double2 w) HC_INL {
+    if constexpr (ACC) w = cadd(w, acc[j]);
+    if constexpr (FINAL) __stcs(dst + j, cscale(w, scale));
+    else dst[j] = w;
+  };
+  if (res) {
+    const double2* U = tb + a.oU + res * a.nu;
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = cmulc(v[c * R0 + Ai], U[Ai]); });
+    });
+  }
+  if constexpr (SYM == SYM_COMPLEX) {
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int b = tid + c * Cfg::T;
+      if (bvalid<Cfg, 0>(c, tid))
+        sfor<R0>([&](auto Ai) HC_INL {
+          const int s = Ns1 * Ai + b;
+          if (s < L) put(s, v[c * R0 + Ai]);
+        });
+    });
+    if (L > B) {
+      sfor<C0>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int b = tid + c * Cfg::T;
+        if (bvalid<Cfg, 0>(c, tid))
+          sfor<R0>([&](auto Ai) HC_INL {
+            const double2 w = v[c * R0 + Ai];
+            int t = 1;
+            for (int j = Ns1 * Ai + b + B; j < L; j += B, ++t) put(j, res ? cmulc(w, Cv[t]) : w);
+          });
+      });
+    }
+  } else {
+    const int H = a.H, LH = L - H, BH = B - H;
+    const double2 c1 = Cv[1];
+    sfor<C0>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int b = tid + c * Cfg::T;
+      if (bvalid<Cfg, 0>(c, tid))
+        sfor<R0>([&](auto Ai) HC_INL {
+          const int s = Ns1 * Ai + b;
+          const double2 w = v[c * R0 + Ai];
+          if (s < LH) put(s + H, w);
+          if (s >= BH) put(s - BH, res ? cmul(w, c1) : w);
+        });
+    });
+  }
+}
+
 // --------------------------------------------------------- conv1d, ping-pong --
 // Two line buffers X and Y per group.  X stages f and then serves f's exchanges (and holds the
 // stashed spectrum F), Y stages g and then serves g's and the inverse's exchanges.  The copy of
@@ -287,7 +404,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
   const GroupSync sync{g + 1, T};
   const AxisDev& a = p.ax;
   stage_tables(tb, a, a.tabn);
-  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const double2* tp = tb;  // host: the ping-pong kernel runs only with every table staged
   if (tid == 0) {
     mbar_init(bar_f, 1);
     mbar_init(bar_g, 1);
@@ -314,7 +431,10 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       // ---- forward f (staged in X, exchanges in X)
       mbar_wait(bar_f, ph_f);
       ph_f ^= 1;
-      if (!(p.dbg & 2)) load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
+      if (!(p.dbg & 2)) {
+        if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
+        else load_pass0_pp<SYM, Cfg>(v, a, tb, X, res, tid);
+      }
       sync();
       fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
         // F kept in registers: X is free right away for the next f line
@@ -331,7 +451,10 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       // ---- forward g (staged in Y, exchanges in Y)
       mbar_wait(bar_g, ph_g);
       ph_g ^= 1;
-      if (!(p.dbg & 2)) load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
+      if (!(p.dbg & 2)) {
+        if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
+        else load_pass0_pp<SYM, Cfg>(v, a, tb, Y, res, tid);
+      }
       sync();
       fft_forward<Cfg>(v, Y, mt, tid, sync, p0);
       if (!(p.dbg & 4)) sfor<CL>([&](auto Ci) HC_INL {
@@ -377,8 +500,18 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
         store_herm<Cfg>(v, a, tp, em, res, tid, Y, sync);
         if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
       } else {
-        if (!(p.dbg & 1)) store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
-        else if (v[0].x == 12345.678) p.out[0] = v[1];  // keep the work alive
+        if (!(p.dbg & 1)) {
+          // acc_y <=> res > 0: the accumulator is staged in Y
+          if (last) {
+            if (acc_y) store_pass0_pp<SYM, Cfg, true, true>(v, a, tb, p.out + base, Y, em.scale, res, tid);
+            else store_pass0_pp<SYM, Cfg, false, true>(v, a, tb, p.out + base, Y, em.scale, res, tid);
+          } else {
+            if (acc_y) store_pass0_pp<SYM, Cfg, true, false>(v, a, tb, slot, Y, 1.0, res, tid);
+            else store_pass0_pp<SYM, Cfg, false, false>(v, a, tb, slot, Y, 1.0, res, tid);
+          }
+        } else if (v[0].x == 12345.678) {
+          p.out[0] = v[1];  // keep the work alive
+        }
         if (acc_y) {
           sync();  // every thread has read its accumulator values from Y
           if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
