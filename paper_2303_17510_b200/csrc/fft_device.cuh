@@ -215,9 +215,16 @@ struct FFTCfg {
   static constexpr int ES = C(P - 1) * RL::R[P - 1];                     // last-pass values per thread
 };
 
+// Barrier objects of the block FFTs.  operator() is a full barrier (read-after-write between
+// an exchange's stores and loads).  The write-after-read hazard (an exchange's loads against
+// the next stores into the same buffer) goes through war_arrive() after the loads and
+// war_wait() before the next stores: a plain barrier in war_arrive() here, a split barrier in
+// SplitSync (kernels.cuh) so that the butterflies between the two overlap the wait.
 // Whole-CTA barrier (column-tile kernels, whose line groups interleave within warps).
 struct CtaSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
+  __device__ __forceinline__ void war_arrive() const { __syncthreads(); }
+  __device__ __forceinline__ void war_wait() const {}
 };
 
 // Group barrier over NT threads (named barrier id; NT must be a multiple of 32).
@@ -226,6 +233,8 @@ struct GroupSync {
   __device__ __forceinline__ void operator()() const {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
   }
+  __device__ __forceinline__ void war_arrive() const { (*this)(); }
+  __device__ __forceinline__ void war_wait() const {}
 };
 
 // Pass-0 twiddles come from a per-butterfly source p0(beta, t0, w): output k of the pass-0
@@ -253,9 +262,11 @@ struct NoHook {
 // last pass's arithmetic -- used to start the next TMA copy into X early.
 // XSTR: element stride of the exchange buffer (1, or G when G line groups interleave their
 // buffers element by element -- column-tile kernels, kernels.cuh)
-template <class Cfg, class Sync, class P0, class Hook = NoHook, int XSTR = 1>
+// hook0() runs after the first exchange (P > 2: before the last one).
+template <class Cfg, class Sync, class P0, class Hook = NoHook, int XSTR = 1, class Hook0 = NoHook>
 __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, const double2* mt, int tid,
-                                            const Sync& sync, const P0& p0, const Hook& hook = Hook()) {
+                                            const Sync& sync, const P0& p0, const Hook& hook = Hook(),
+                                            const Hook0& hook0 = Hook0()) {
   constexpr int P = Cfg::P, T = Cfg::T;
   static_assert(P >= 2, "radix plans have at least two passes");
   sfor<P>([&](auto I) HC_INL {
@@ -279,6 +290,7 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
     });
     if constexpr (i < P - 1) {
       constexpr int St = Cfg::St(i + 1);
+      sync.war_wait();
       sfor<C>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
@@ -297,7 +309,8 @@ __device__ __forceinline__ void fft_forward(double2 (&v)[Cfg::E], double2* X, co
           sfor<R2>([&](auto Ai) HC_INL { v[c * R2 + Ai] = X[(K * St + Ns2 * Ai + b) * XSTR]; });
         }
       });
-      sync();
+      sync.war_arrive();
+      if constexpr (i == 0) hook0();
       if constexpr (i == P - 2) hook();
     }
   });
@@ -400,6 +413,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
     });
     if constexpr (i > 0) {
       constexpr int St = Cfg::St(i);
+      sync.war_wait();
       sfor<C>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         const int beta = tid + c * T;
@@ -419,7 +433,7 @@ __device__ __forceinline__ void fft_inverse(double2 (&v)[Cfg::E], double2* X, co
           sfor<R0>([&](auto Ki) HC_INL { v[c * R0 + Ki] = X[((K + Rp0 * Ki) * St + b) * XSTR]; });
         }
       });
-      sync();
+      sync.war_arrive();
       if constexpr (i == 1) hook();
     }
   });

@@ -326,7 +326,9 @@ __device__ __forceinline__ void load_pass0_pp(double2 (&v)[Cfg::E], const AxisDe
 
 // dst[j] = (ACC ? acc[j] : 0) + w_j, times `scale` with streaming stores when FINAL; acc is the
 // residue accumulator staged in shared memory (unit stride), dst a unit-stride line.
-template <int SYM, class Cfg, bool ACC, bool FINAL>
+// SMEM: dst is a shared-memory line (possibly == acc, updated in place) that a bulk copy
+// writes out afterwards.
+template <int SYM, class Cfg, bool ACC, bool FINAL, bool SMEM = false>
 __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisDev& a, const double2* tb, double2* dst,
                                                const double2* acc, double scale, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
@@ -334,7 +336,8 @@ __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisD
   const double2* Cv = tb + a.oC + res * a.nc;
   auto put = [&](int j, double2 w) HC_INL {
     if constexpr (ACC) w = cadd(w, acc[j]);
-    if constexpr (FINAL) __stcs(dst + j, cscale(w, scale));
+    if constexpr (FINAL) w = cscale(w, scale);
+    if constexpr (FINAL && !SMEM) __stcs(dst + j, w);
     else dst[j] = w;
   };
   if (res) {
@@ -384,6 +387,9 @@ __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisD
 }
 
 // --------------------------------------------------------- conv1d, ping-pong --
+#ifndef HC_PP_BULK
+#define HC_PP_BULK 1
+#endif
 // Two line buffers X and Y per group.  X stages f and then serves f's exchanges (and holds the
 // stashed spectrum F), Y stages g and then serves g's and the inverse's exchanges.  The copy of
 // the next f line into X starts as soon as F has been consumed by the product, the next g line
@@ -420,9 +426,23 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
     tma_copy(X, p.f + p.lin.base(item), row_bytes, bar_f);
     tma_copy(Y, p.g + p.lin.base(item), row_bytes, bar_g);
   }
+  // complex / centered: each residue's output is assembled in Y and written out by a bulk
+  // copy (the SM moves on while it drains); the next g copy into Y waits for its reads
+  constexpr bool BULK = SYM != SYM_HERMITIAN && HC_PP_BULK;
+  const double2* g_next = nullptr;  // pending next-g copy (issued once the bulk store read Y)
+  const bool tr = p.trace && blockIdx.x == 0 && threadIdx.x == 0;
+  int tn = 0;
+#define HC_TRACE()                                   \
+  do {                                               \
+    if (p.trace) {                                   \
+      sync();                                        \
+      if (tr && tn < 256) p.trace[tn++] = clock64(); \
+    }                                                \
+  } while (0)
   for (; item < p.lin.count; item += step) {
     const long long base = p.lin.base(item);
     for (int res = 0; res < a.n; ++res) {
+      HC_TRACE();
       const bool last = res == a.n - 1;
       const long long nbase = !last ? base : (item + step < p.lin.count ? p.lin.base(item + step) : -1);
       double2 v[Cfg::E];
@@ -431,15 +451,26 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       // ---- forward f (staged in X, exchanges in X)
       mbar_wait(bar_f, ph_f);
       ph_f ^= 1;
+      HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
         else load_pass0_pp<SYM, Cfg>(v, a, tb, X, res, tid);
       }
       sync();
-      fft_forward<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
+      HC_TRACE();
+      auto hk = [&]() HC_INL {
         // F kept in registers: X is free right away for the next f line
         if (STASH_REGS && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
-      });
+      };
+      auto hk0 = [&]() HC_INL {
+        // the previous residue's bulk store has had a load and a pass to read Y
+        if (BULK && g_next && tid == 0) {
+          bulk_wait_read();
+          tma_copy(Y, g_next, row_bytes, bar_g);
+        }
+      };
+      fft_forward<Cfg, GroupSync, P0Res<SYM>, decltype(hk), 1, decltype(hk0)>(v, X, mt, tid, sync, p0, hk, hk0);
+      if constexpr (BULK) g_next = nullptr;
       sfor<CL>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
@@ -448,15 +479,19 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
             else X[Ki * NBL + tid + c * T] = v[c * RL + Ki];
           });
       });
+      HC_TRACE();
       // ---- forward g (staged in Y, exchanges in Y)
       mbar_wait(bar_g, ph_g);
       ph_g ^= 1;
+      HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
         else load_pass0_pp<SYM, Cfg>(v, a, tb, Y, res, tid);
       }
       sync();
+      HC_TRACE();
       fft_forward<Cfg>(v, Y, mt, tid, sync, p0);
+      HC_TRACE();
       if (!(p.dbg & 4)) sfor<CL>([&](auto Ci) HC_INL {
         constexpr int c = Ci;
         if (bvalid<Cfg, Cfg::P - 1>(c, tid))
@@ -479,26 +514,48 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       const bool acc_y = SYM != SYM_HERMITIAN && res > 0;
       auto release_y = [&]() HC_INL {
         if (SYM != SYM_HERMITIAN && tid == 0) {
-          if (acc_y) tma_copy(Y, slot, row_bytes, bar_g);
-          else if (nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+          if (acc_y) {
+            if constexpr (BULK) bulk_wait_all();  // the slot's bulk store has landed
+            tma_copy(Y, slot, row_bytes, bar_g);
+          } else if (!BULK && nbase >= 0) {
+            tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+          }
         }
       };
+      HC_TRACE();
       if (!(p.dbg & 8)) {
         fft_inverse<Cfg>(v, Y, mt, tid, sync, p0, release_y);
       } else {
         sync();
         release_y();
       }
+      HC_TRACE();
       const double2* acc = res > 0 ? slot : nullptr;
       if (acc_y) {
         mbar_wait(bar_g, ph_g);
         ph_g ^= 1;
         acc = Y;
       }
+      HC_TRACE();
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
         store_herm<Cfg>(v, a, tp, em, res, tid, Y, sync);
         if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+      } else if constexpr (BULK) {
+        // acc_y <=> res > 0: the accumulator is staged in Y, updated in place
+        if (!(p.dbg & 1)) {
+          if (last) {
+            if (acc_y) store_pass0_pp<SYM, Cfg, true, true, true>(v, a, tb, Y, Y, em.scale, res, tid);
+            else store_pass0_pp<SYM, Cfg, false, true, true>(v, a, tb, Y, Y, em.scale, res, tid);
+          } else {
+            if (acc_y) store_pass0_pp<SYM, Cfg, true, false, true>(v, a, tb, Y, Y, 1.0, res, tid);
+            else store_pass0_pp<SYM, Cfg, false, false, true>(v, a, tb, Y, Y, 1.0, res, tid);
+          }
+        }
+        fence_proxy_async_smem();
+        sync();
+        if (tid == 0) tma_store(last ? p.out + base : slot, Y, row_bytes, last);
+        g_next = nbase >= 0 ? p.g + nbase : nullptr;
       } else {
         if (!(p.dbg & 1)) {
           // acc_y <=> res > 0: the accumulator is staged in Y
@@ -519,6 +576,8 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       }
     }
   }
+  if (BULK && tid == 0) bulk_wait_all();  // shared memory stays valid until the last store read it
+#undef HC_TRACE
 }
 
 // ------------------------------------------------------------- conv1d, paired --

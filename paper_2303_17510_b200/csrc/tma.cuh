@@ -60,6 +60,45 @@ __device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t by
   }
 }
 
+// ---- shared -> global bulk stores (bulk-group completion) ----
+// Each thread that wrote the source through ordinary stores runs fence_proxy_async_smem(), then
+// the group synchronises, then one thread issues the copy and commits the group.  Before the
+// source is overwritten, the same thread waits with bulk_wait_read().
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
+// bytes: multiple of 16, both addresses 16-B aligned; evict_first: streaming output
+__device__ __forceinline__ void tma_store(void* dst, const void* src, uint32_t bytes, bool evict_first) {
+  constexpr uint32_t kChunk = 32768;
+  const uint64_t pol = l2_policy_evict_first();
+  for (uint32_t off = 0; off < bytes; off += kChunk) {
+    const uint32_t n = bytes - off < kChunk ? bytes - off : kChunk;
+    if (evict_first)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                       static_cast<char*>(dst) + off),
+                   "r"(smem_u32(static_cast<const char*>(src) + off)), "r"(n), "l"(pol)
+                   : "memory");
+    else
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(static_cast<char*>(dst) + off),
+                   "r"(smem_u32(static_cast<const char*>(src) + off)), "r"(n)
+                   : "memory");
+  }
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// all committed bulk stores of this thread have finished reading shared memory
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+
+// all committed bulk stores of this thread are complete (their global writes performed)
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // Warm L2 with a line that will be staged later (no shared-memory destination, no barrier).
 __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
   constexpr uint32_t kChunk = 32768;
