@@ -202,16 +202,19 @@ void build_tables(AxisPlan& ap) {
   a.ns1 = ns1;
   a.nu = nu;
   a.nc = nc;
-  // order: MT U C A Z H Bl Bh (block_io.cuh); the kernels stage the prefix that fits
+  // order: MT U C A Z H Bl Bh (block_io.cuh); the kernels stage the prefix that fits.  The
+  // residue-indexed tables U C Z H omit row v = 0 (every kernel skips those factors at v = 0):
+  // their offsets point one row before the first stored row.
   a.oMT = 0;
-  a.oU = k->mt;
-  a.oC = a.oU + n * nu;
-  a.oA = a.oC + n * nc;
-  a.oZ = a.oA + ns1;
-  a.oH = a.oZ + n * ns1;
-  a.oBl = a.oH + n;
+  const int rU = k->mt, rC = rU + (n - 1) * nu, rA = rC + (n - 1) * nc, rZ = rA + ns1, rH = rZ + (n - 1) * ns1;
+  a.oU = rU - nu;
+  a.oC = rC - nc;
+  a.oA = rA;
+  a.oZ = rZ - ns1;
+  a.oH = rH - 1;
+  a.oBl = rH + (n - 1);
   a.oBh = a.oBl + ns1;
-  ap.tab_full = a.sym == hc::SYM_HERMITIAN ? a.oBh + R0 + 1 : a.oH;
+  ap.tab_full = a.sym == hc::SYM_HERMITIAN ? a.oBh + R0 + 1 : rH;
   a.tabn = ap.tab_full;
   a.tabfull = ap.tab_full;
   const int total = a.oBh + R0 + 1;
@@ -235,7 +238,7 @@ void build_tables(AxisPlan& ap) {
     return make_double2(c.real(), c.imag());
   };
   for (int b = 0; b < ns1; ++b) h[a.oA + b] = z(Bc, b);
-  for (int v = 0; v < n; ++v) {
+  for (int v = 1; v < n; ++v) {
     for (int b = 0; b < ns1; ++b) h[a.oZ + v * ns1 + b] = z(qm, (long long)v * b);
     for (int i = 0; i < nu; ++i) h[a.oU + v * nu + i] = z(qm, (long long)v * ns1 * i);
     for (int t = 0; t < nc; ++t) h[a.oC + v * nc + t] = z(qm, (long long)v * t * B);
@@ -252,7 +255,7 @@ void build_tables(AxisPlan& ap) {
     for (int kk = 1; kk < k->R[i]; ++kk)
       for (long long b = 0; b < Nsi1; ++b) h[o++] = z(Nsi, b * kk);
   }
-  if (o != a.oU) throw std::logic_error("table size mismatch");
+  if (o != k->mt) throw std::logic_error("table size mismatch");
   double2* dp = nullptr;
   CK(cudaMalloc(&dp, (size_t)total * sizeof(double2)));
   CK(cudaMemcpy(dp, h.data(), (size_t)total * sizeof(double2), cudaMemcpyHostToDevice));

@@ -277,7 +277,7 @@ __device__ __forceinline__ void load_pass0_pp(double2 (&v)[Cfg::E], const AxisDe
                                               const double2* X, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
   const int L = a.L, B = a.B;
-  const double2* Cv = tb + a.oC + res * a.nc;
+  const double2* Cv = tb + (a.oC + res * a.nc);  // row res (rows from 1, see build_tables)
   if constexpr (SYM == SYM_COMPLEX) {
     sfor<C0>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
@@ -302,7 +302,7 @@ __device__ __forceinline__ void load_pass0_pp(double2 (&v)[Cfg::E], const AxisDe
     }
   } else {
     const int H = a.H, LH = L - H, BH = B - H;
-    const double2 c1 = Cv[1];
+    const double2 c1 = res ? Cv[1] : make_double2(1.0, 0.0);
     sfor<C0>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int b = tid + c * Cfg::T;
@@ -316,7 +316,7 @@ __device__ __forceinline__ void load_pass0_pp(double2 (&v)[Cfg::E], const AxisDe
     });
   }
   if (res) {
-    const double2* U = tb + a.oU + res * a.nu;
+    const double2* U = tb + (a.oU + res * a.nu);
     sfor<C0>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = cmul(v[c * R0 + Ai], U[Ai]); });
@@ -333,7 +333,7 @@ __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisD
                                                const double2* acc, double scale, int res, int tid) {
   constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
   const int L = a.L, B = a.B;
-  const double2* Cv = tb + a.oC + res * a.nc;
+  const double2* Cv = tb + (a.oC + res * a.nc);  // row res (rows from 1, see build_tables)
   auto put = [&](int j, double2 w) HC_INL {
     if constexpr (ACC) w = cadd(w, acc[j]);
     if constexpr (FINAL) w = cscale(w, scale);
@@ -341,7 +341,7 @@ __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisD
     else dst[j] = w;
   };
   if (res) {
-    const double2* U = tb + a.oU + res * a.nu;
+    const double2* U = tb + (a.oU + res * a.nu);
     sfor<C0>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = cmulc(v[c * R0 + Ai], U[Ai]); });
@@ -371,7 +371,7 @@ __device__ __forceinline__ void store_pass0_pp(double2 (&v)[Cfg::E], const AxisD
     }
   } else {
     const int H = a.H, LH = L - H, BH = B - H;
-    const double2 c1 = Cv[1];
+    const double2 c1 = res ? Cv[1] : make_double2(1.0, 0.0);
     sfor<C0>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int b = tid + c * Cfg::T;

@@ -7,6 +7,12 @@
 #pragma once
 #include <cstdint>
 
+// HC_TMA_FENCE=1: a generic->async proxy fence before every bulk load (off by default: every
+// load is issued after a group barrier that follows the buffer's last generic accesses -- its
+// loads have returned and its stores have been performed in shared memory; measured 2% of c2)
+#ifndef HC_TMA_FENCE
+#define HC_TMA_FENCE 0
+#endif
 namespace hc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -52,7 +58,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 // Called by a single thread.
 __device__ __forceinline__ void tma_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   constexpr uint32_t kChunk = 32768;
-  fence_proxy_async();
+  if (HC_TMA_FENCE) fence_proxy_async();
   mbar_expect_tx(bar, bytes);
   for (uint32_t off = 0; off < bytes; off += kChunk) {
     const uint32_t n = bytes - off < kChunk ? bytes - off : kChunk;

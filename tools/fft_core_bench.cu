@@ -77,16 +77,9 @@ void run(const char* name) {
 }
 
 int main() {
-  run<FFTCfg<Radices<16, 16, 16>, 256>, 2>("16x16x16");
-  run<FFTCfg<Radices<16, 16, 12>, 192>, 2>("16x16x12");
-  run<FFTCfg<Radices<16, 16, 12>, 256>, 2>("16x16x12/256");
-  run<FFTCfg<Radices<16, 16, 24>, 384>, 2>("16x16x24");
   run<FFTCfg<Radices<16, 16, 24>, 384>>("16x16x24");
+  run<FFTCfg<Radices<16, 24, 16>, 384>>("16x24x16");
   run<FFTCfg<Radices<24, 16, 16>, 384>>("24x16x16");
-  run<FFTCfg<Radices<8, 8, 8, 12>, 768>>("8x8x8x12");
   run<FFTCfg<Radices<16, 16, 16>, 256>>("16x16x16");
-  run<FFTCfg<Radices<16, 16, 12>, 192>>("16x16x12");
-  run<FFTCfg<Radices<16, 16, 8>, 128>>("16x16x8");
-  run<FFTCfg<Radices<8, 8, 8>, 64>>("8x8x8");
   return 0;
 }
