@@ -120,6 +120,14 @@ size_t hconv_plan_workspace_bytes(const hconv_plan* plan);
  * CUDA library: device pointers, asynchronous on stream (cudaStream_t, NULL = legacy).
  * Oracle: host pointers, stream ignored.                                           */
 hconv_status hconv_convolve(hconv_plan* plan, const void* const* in, void* const* out, void* stream);
+/* Host-buffer convolution -- the reference library's own calling convention (host arrays,
+ * synchronous).  in[A], out[B]: HOST complex128 arrays with the stored
+ * layout of the descriptor; out[b] == in[b] allowed.  CUDA library: a 1D batch streams through
+ * the device in chunks of copies (HCONV_HOST_CHUNKS, default 8) -- the host->device copies, the
+ * convolution and the device->host copies of consecutive chunks overlap on three streams
+ * (page-locked host memory required for the overlap); N-D plans copy in, convolve, copy out.
+ * Oracle: same as hconv_convolve.                                                            */
+hconv_status hconv_convolve_host(hconv_plan* plan, const void* const* in, void* const* out);
 hconv_status hconv_plan_destroy(hconv_plan* plan);
 const char* hconv_last_error(void);
 /* Library identity: "cuda-sm_100a" or "oracle-cpu". */

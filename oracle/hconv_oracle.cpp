@@ -863,6 +863,11 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
     }
   });
 }
+
+// host arrays already: the oracle's convolve is synchronous on host memory
+hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* const* out) {
+  return hconv_convolve(p, in, out, nullptr);
+}
 hconv_status hconv_plan_destroy(hconv_plan* p) { delete p; return HCONV_OK; }
 
 // ---- oracle-only entry points (tests and bench cpu_baseline) ----

@@ -68,6 +68,7 @@ PROTOTYPES = {
     "hconv_plan_params": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Params)]),
     "hconv_plan_workspace_bytes": (C.c_size_t, [C.c_void_p]),
     "hconv_convolve": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p]),
+    "hconv_convolve_host": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
     "hconv_plan_destroy": (C.c_int, [C.c_void_p]),
     "hconv_last_error": (C.c_char_p, []),
     "hconv_backend": (C.c_char_p, []),

@@ -658,6 +658,54 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
 }  // namespace
 
 // ------------------------------------------------------------------ plan ----
+// Device side of hconv_convolve_host: three streams (host->device, compute, device->host),
+// three slots of input/output chunks, created on first use.
+struct HostPipe {
+  static constexpr int kSlots = 3;
+  cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+  cudaEvent_t loaded[kSlots] = {}, done[kSlots] = {}, drained[kSlots] = {};
+  double2* buf[kSlots][2] = {};  // per slot: input 0 (also the output, in place) and input 1
+  size_t elems = 0;              // per buffer
+  int nslots = 0;                // slots allocated
+  bool ready = false;
+  void init() {
+    if (ready) return;
+    for (auto& s : st) CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (int k = 0; k < kSlots; ++k) {
+      CK(cudaEventCreateWithFlags(&loaded[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&drained[k], cudaEventDisableTiming));
+    }
+    ready = true;
+  }
+  void ensure(size_t n, int slots) {
+    if (n <= elems && slots <= nslots) return;
+    for (auto& sl : buf)
+      for (auto& b : sl) {
+        if (b) CK(cudaFree(b));
+        b = nullptr;
+      }
+    elems = 0;
+    nslots = 0;
+    for (int k = 0; k < slots; ++k)
+      for (auto& b : buf[k]) CK(cudaMalloc(&b, n * sizeof(double2)));
+    elems = n;
+    nslots = slots;
+  }
+  ~HostPipe() {
+    for (auto& sl : buf)
+      for (auto& b : sl)
+        if (b) cudaFree(b);
+    if (!ready) return;
+    for (int k = 0; k < kSlots; ++k) {
+      cudaEventDestroy(loaded[k]);
+      cudaEventDestroy(done[k]);
+      cudaEventDestroy(drained[k]);
+    }
+    for (auto& s : st) cudaStreamDestroy(s);
+  }
+};
+
 struct hconv_plan {
   hconv_desc d{};
   int device = 0;
@@ -666,6 +714,7 @@ struct hconv_plan {
   std::vector<double2*> buffers;      // N-D work / accumulator buffers
   std::vector<long long> chunk;               // per level: arrays processed per pass (L2 blocking)
   PlanReport report;
+  HostPipe host;                      // hconv_convolve_host
   ~hconv_plan() {
     scratch.release();
     for (double2* b : buffers)
@@ -1054,6 +1103,55 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
       launch_conv(ap, lin, ins[0], ins[1], (double2*)out[0], p->scratch, s);
     } else {
       nd_level(p, 0, 1, ins, (double2*)out[0], s);
+    }
+  });
+}
+
+hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* const* out) {
+  return guarded([&] {
+    if (!p || !in || !out || !in[0] || !in[1] || !out[0]) throw std::invalid_argument("null argument");
+    CK(cudaSetDevice(p->device));
+    HostPipe& hp = p->host;
+    hp.init();
+    const char* hin[2] = {(const char*)in[0], (const char*)in[1]};
+    char* hout = (char*)out[0];
+    if (p->d.dims == 1) {
+      const AxisPlan& ap = p->ax[0];
+      const long long C = (long long)(p->d.C ? p->d.C : 1), S = (long long)ap.data;
+      const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
+      const long long want = std::getenv("HCONV_HOST_CHUNKS") ? std::atoll(std::getenv("HCONV_HOST_CHUNKS")) : 8;
+      const long long nch = std::max<long long>(1, std::min<long long>(C, want));
+      const long long per = (C + nch - 1) / nch;
+      hp.ensure((size_t)((per - 1) * dist + S), (int)std::min<long long>(nch, HostPipe::kSlots));
+      int slot = 0;
+      for (long long c0 = 0; c0 < C; c0 += per, slot = (slot + 1) % HostPipe::kSlots) {
+        const long long cnt = std::min(per, C - c0);
+        const size_t bytes = (size_t)((cnt - 1) * dist + S) * sizeof(double2);
+        const size_t off = (size_t)(c0 * dist) * sizeof(double2);
+        double2* const* b = hp.buf[slot];
+        // slot reuse: its previous chunk has been copied back
+        CK(cudaStreamWaitEvent(hp.st[0], hp.drained[slot], 0));
+        for (int a = 0; a < 2; ++a) CK(cudaMemcpyAsync(b[a], hin[a] + off, bytes, cudaMemcpyHostToDevice, hp.st[0]));
+        CK(cudaEventRecord(hp.loaded[slot], hp.st[0]));
+        CK(cudaStreamWaitEvent(hp.st[1], hp.loaded[slot], 0));
+        const hc::Lines lin{cnt, 1, dist, 0, 1};
+        launch_conv(ap, lin, b[0], b[1], b[0], p->scratch, hp.st[1]);
+        CK(cudaEventRecord(hp.done[slot], hp.st[1]));
+        CK(cudaStreamWaitEvent(hp.st[2], hp.done[slot], 0));
+        CK(cudaMemcpyAsync(hout + off, b[0], bytes, cudaMemcpyDeviceToHost, hp.st[2]));
+        CK(cudaEventRecord(hp.drained[slot], hp.st[2]));
+      }
+      CK(cudaStreamSynchronize(hp.st[2]));
+    } else {
+      size_t n = 1;
+      for (const AxisPlan& ap : p->ax) n *= ap.data;
+      hp.ensure(n, 1);
+      double2* const* b = hp.buf[0];
+      for (int a = 0; a < 2; ++a) CK(cudaMemcpyAsync(b[a], hin[a], n * sizeof(double2), cudaMemcpyHostToDevice, hp.st[1]));
+      const double2* ins[2] = {b[0], b[1]};
+      nd_level(p, 0, 1, ins, b[0], hp.st[1]);
+      CK(cudaMemcpyAsync(hout, b[0], n * sizeof(double2), cudaMemcpyDeviceToHost, hp.st[1]));
+      CK(cudaStreamSynchronize(hp.st[1]));
     }
   });
 }

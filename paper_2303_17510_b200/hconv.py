@@ -267,6 +267,11 @@ class _Plan:
         outs = (C.c_void_p * 1)(out.data_ptr())
         _check(lib().hconv_convolve(self._h, ins, outs, _stream(stream)))
 
+    def _run_host(self, inputs: Sequence[torch.Tensor], out: torch.Tensor) -> None:
+        ins = (C.c_void_p * len(inputs))(*[t.data_ptr() for t in inputs])
+        outs = (C.c_void_p * 1)(out.data_ptr())
+        _check(lib().hconv_convolve_host(self._h, ins, outs))
+
 
 class Conv1dPlan(_Plan):
     """1D dealiased convolution of C copies ([C, dist] complex128 rows).
@@ -351,6 +356,35 @@ def convolve_nd(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: ConvPl
             raise ValueError(f"expected shape {shp}, got {tuple(t.shape)}")
     o = ins[0] if out is None else _dev(out)
     plan._run(ins, o, stream)
+    return [o]
+
+
+def _host(t: torch.Tensor) -> torch.Tensor:
+    if t.is_cuda or t.dtype != torch.complex128 or not t.is_contiguous():
+        raise ValueError("convolve_host expects contiguous complex128 CPU tensors")
+    return t
+
+
+def convolve_host(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: "_Plan",
+                  out: Optional[torch.Tensor] = None) -> list[torch.Tensor]:
+    """convolve / convolve_nd on HOST tensors -- the reference library's calling convention
+    (synchronous, host arrays).  The library streams a 1D batch through the device in chunks,
+    overlapping host->device copies, the convolution and device->host copies (pin the tensors,
+    ``t.pin_memory()``, for the overlap).  Computes on the GPU; there is no CPU path."""
+    _check_mult(inputs, mult, plan)
+    ins = [_host(t) for t in inputs]
+    if isinstance(plan, ConvPlanND):
+        shp = plan.shape()
+        for t in ins:
+            if tuple(t.shape) != shp:
+                raise ValueError(f"expected shape {shp}, got {tuple(t.shape)}")
+    else:
+        need = (plan.desc.C - 1) * (plan.desc.dist or plan.params.dataLength()) + plan.params.dataLength()
+        for t in ins:
+            if t.numel() < need:
+                raise ValueError("input smaller than the plan's C x dist layout")
+    o = ins[0] if out is None else _host(out)
+    plan._run_host(ins, o)
     return [o]
 
 

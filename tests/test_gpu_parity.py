@@ -213,6 +213,40 @@ def test_config2_hybrid_plans(cuda, oracle, m):
     _check_conv(out, ref, fn, gn)
 
 
+@pytest.mark.parametrize("C_,chunks", [(4096, "8"), (1000, "3"), (5, "8"), (1, "8")])
+def test_convolve_host_matches_device(cuda, C_, chunks, monkeypatch):
+    """hconv_convolve_host (host arrays, chunked H2D / convolve / D2H on three streams) gives
+    bit-identical results to the device-pointer call: same kernels on the same lines."""
+    import torch
+
+    monkeypatch.setenv("HCONV_HOST_CHUNKS", chunks)
+    L, M = 6000, 11999
+    f, g = _inputs(cuda, (C_, L), 5)
+    plan = cuda.Conv1dPlan(L, M, 6144, C_=C_)
+    dev = cuda.convolve([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu()
+    hf, hg = f.cpu().pin_memory(), g.cpu().pin_memory()
+    ho = torch.empty_like(hf).pin_memory()
+    cuda.convolve_host([hf, hg], plan.mult, plan, out=ho)
+    assert torch.equal(ho, dev)
+    # in place (the reference's convention): the result overwrites input 0
+    cuda.convolve_host([hf, hg], plan.mult, plan)
+    assert torch.equal(hf, dev)
+
+
+def test_convolve_host_nd(cuda):
+    import torch
+
+    L, M = 256, 511
+    f, g = _inputs(cuda, (L, L), 6)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(L, M, 512), cuda.AxisSpec(L, M, 512)])
+    dev = cuda.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu()
+    ho = torch.empty(L, L, dtype=torch.complex128)
+    cuda.convolve_host([f.cpu(), g.cpu()], plan.mult, plan, out=ho)
+    assert torch.equal(ho, dev)
+    with pytest.raises(ValueError):
+        cuda.convolve_host([f, g], plan.mult, plan)  # device tensors are rejected
+
+
 @pytest.mark.parametrize("seed", [1, 2, 3])
 def test_config3_full(cuda, oracle, seed):
     """Hermitian K=8192 (L=16383), M=24574, batch 2048; Im f_0 = 0."""
