@@ -405,6 +405,7 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   CK(cudaGetLastError());
   if (tbuf) {
     unsigned long long h[256];
+    CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost));
     std::fprintf(stderr, "[hconv trace %s grid %d]", ap.k->radix, grid);
     for (int i = 1; i < 256 && h[i]; ++i) std::fprintf(stderr, " %llu", h[i] - h[i - 1]);
