@@ -116,6 +116,11 @@ def _conv_cases():
             cases.append((0, Bc - 1, 2 * Bc - 1, Bc // 4))        # inner p = 4
         cases.append((1, 2 * Bc - 1, 3 * Bc - 2, Bc))
         cases.append((2, 4 * Bc - 1, 6 * Bc - 2, 2 * Bc))
+        # unfolded lines (L <= B; the residue accumulator of the large kernels lives in TMEM),
+        # two and three residues
+        cases.append((0, Bc, 3 * Bc - 1, Bc))
+        cases.append((1, Bc - 1, (3 * Bc - 2) // 2, Bc))
+        cases.append((1, Bc - 1, 3 * Bc, Bc))
     return cases
 
 
