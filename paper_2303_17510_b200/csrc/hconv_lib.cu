@@ -365,10 +365,11 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
       c.stage = 1;
     } else if (k->pair) {
       c.stage = 0;  // the paired kernel stages both lines into X and Y or none
-    } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + S)) * sizeof(double2) <= kSmemCap) {
+    } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + std::max(S, ap.dev.Bc))) * sizeof(double2) <= kSmemCap) {
+      // (the Hermitian packing writes Z'_k, k < Bc, into the staged line in place)
       c.stage = 2;
       c.in_off = c.gs;
-      c.gs += S;
+      c.gs += std::max(S, ap.dev.Bc);
     }
   }
   c.tabn = staged_tabn(ap, c.gs);

@@ -121,6 +121,59 @@ __device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const Axi
   sync();
 }
 
+// Hermitian pass-0 input from a line staged in shared memory: the packed values Z'_k
+// (load_Zp_fast) are built IN PLACE, one quad {k, Bc-k, Bc+k, B-k} per thread -- the quad's four
+// stored values are read before its two outputs Z'_k, Z'_{Bc-k} are written, and quads are
+// disjoint -- so each W_s is formed once (load_Zp_fast forms it twice) with int offsets:
+//   W_s = (f_s + conj f_{B-s} [zeta^{-vB}]) zeta^{vs},  e = W_k + conj W_{Bc-k},
+//   o = (W_k - conj W_{Bc-k}) zeta_B^k,  Z'_k = e + i o,  Z'_{Bc-k} = conj e + i conj o.
+// The caller synchronises before reading Z' in pass-0 layout (load_plain).
+template <int NT>
+__device__ __forceinline__ void herm_pack(double2* X, const AxisDev& a, const double2* tb, int v, int tid) {
+  const int Bc = a.Bc, B = a.B, S = a.S, half = Bc / 2, ns1 = a.ns1;
+  const double2 one = make_double2(1.0, 0.0);
+  const double2 cH = v ? tb[a.oH + v] : one;            // zeta_qm^{v Bc}
+  const double2 c1 = v ? tb[a.oC + v * a.nc + 1] : one;  // zeta_qm^{v B}
+  const double2* Zr = tb + (a.oZ + v * ns1);
+  const double2* Ur = tb + (a.oU + v * a.nu);
+  const double2* Bl = tb + a.oBl;
+  const double2* Bh = tb + a.oBh;
+  for (int k = tid; k <= half; k += NT) {
+    const int kh = k / ns1, kl = k - kh * ns1;
+    const int s2 = Bc - k;
+    double2 x1 = k < S ? X[k] : make_double2(0.0, 0.0);
+    double2 x2 = s2 < S ? X[s2] : make_double2(0.0, 0.0);
+    const int r1 = B - k, r2 = B - s2;  // r1 > 0 always (k <= Bc/2 < B)
+    const double2 y1 = r1 < S ? cconj(X[r1]) : make_double2(0.0, 0.0);
+    const double2 y2 = (r2 > 0 && r2 < S) ? cconj(X[r2]) : make_double2(0.0, 0.0);
+    double2 wk, wm;
+    if (v) {
+      const double2 zk = cmul(Zr[kl], Ur[kh]);  // zeta_qm^{v k}
+      const double2 zm = cmulc(cH, zk);         // zeta_qm^{v (Bc - k)}
+      wk = cmul(cadd(x1, cmulc(y1, c1)), zk);
+      wm = cconj(cmul(cadd(x2, cmulc(y2, c1)), zm));
+    } else {
+      wk = cadd(x1, y1);
+      wm = cconj(cadd(x2, y2));
+    }
+    const double2 e = cadd(wk, wm);
+    const double2 o = cmul(csub(wk, wm), cmul(Bh[kh], Bl[kl]));  // zeta_B^k
+    X[k] = make_double2(e.x - o.y, e.y + o.x);
+    if (k != 0 && k != half) X[s2] = make_double2(e.x + o.y, o.x - e.y);
+  }
+}
+
+// pass-0 values straight from a shared-memory line in natural order (v[c R0 + a] = X[Ns1 a + b])
+template <class Cfg>
+__device__ __forceinline__ void load_plain(double2 (&v)[Cfg::E], const double2* X, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
+  sfor<C0>([&](auto Ci) HC_INL {
+    constexpr int c = Ci;
+    const int b = tid + c * Cfg::T;
+    if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = X[Ns1 * Ai + b]; });
+  });
+}
+
 // stage the per-axis tables (block_io.cuh: A Z U C MT [H Bl Bh]) into shared memory (whole CTA)
 __device__ __forceinline__ void stage_tables(double2* tb, const AxisDev& a, int n) {
   for (int i = threadIdx.x; i < n; i += blockDim.x) tb[i] = __ldg(a.tab + i);
@@ -195,7 +248,13 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
           mbar_wait(bar_in, ph_in);
           ph_in ^= 1;
           HC_TRACE();
-          load_pass0<SYM, Cfg>(v, a, tp, IN, 1, res, tid);
+          if constexpr (SYM == SYM_HERMITIAN) {
+            herm_pack<T>(IN, a, tp, res, tid);
+            sync();
+            load_plain<Cfg>(v, IN, tid);
+          } else {
+            load_pass0<SYM, Cfg>(v, a, tp, IN, 1, res, tid);
+          }
           sync();  // IN (X in mode 1) fully read before the exchange writes / the next copy
           if (stage == 2 && tid == 0 && nxt) tma_copy(IN, nxt, row_bytes, bar_in);
         } else {
@@ -531,8 +590,13 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       ph_f ^= 1;
       HC_TRACE();
       if (!(p.dbg & 2)) {
-        if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
-        else load_pass0_pp<SYM, Cfg>(v, a, tb, X, res, tid);
+        if constexpr (SYM == SYM_HERMITIAN) {
+          herm_pack<T>(X, a, tb, res, tid);
+          sync();
+          load_plain<Cfg>(v, X, tid);
+        } else {
+          load_pass0_pp<SYM, Cfg>(v, a, tb, X, res, tid);
+        }
       }
       sync();
       HC_TRACE();
@@ -564,8 +628,13 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       ph_g ^= 1;
       HC_TRACE();
       if (!(p.dbg & 2)) {
-        if constexpr (SYM == SYM_HERMITIAN) load_pass0<SYM, Cfg>(v, a, tp, Y, 1, res, tid);
-        else load_pass0_pp<SYM, Cfg>(v, a, tb, Y, res, tid);
+        if constexpr (SYM == SYM_HERMITIAN) {
+          herm_pack<T>(Y, a, tb, res, tid);
+          sync();
+          load_plain<Cfg>(v, Y, tid);
+        } else {
+          load_pass0_pp<SYM, Cfg>(v, a, tb, Y, res, tid);
+        }
       }
       sync();
       HC_TRACE();
