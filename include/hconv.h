@@ -53,8 +53,24 @@ typedef enum hconv_status {
 typedef enum hconv_symmetry { HCONV_COMPLEX = 0, HCONV_CENTERED = 1, HCONV_HERMITIAN = 2 } hconv_symmetry;
 /* plan.hpp:20 enum class Regime { P1, P2, Inner } */
 typedef enum hconv_regime { HCONV_P1 = 0, HCONV_P2 = 1, HCONV_INNER = 2 } hconv_regime;
-/* SPEC.md:424 builtin_mult_product: B = 1, elementwise product of the A inputs */
-typedef enum hconv_mult { HCONV_MULT_PRODUCT = 0 } hconv_mult;
+/* SPEC.md:396-399 MultOperator, SPEC.md:424 builtin_mult_product */
+typedef enum hconv_mult {
+  HCONV_MULT_PRODUCT = 0,  /* builtin_mult_product(A): B = 1, elementwise product of the A >= 2 inputs */
+  HCONV_MULT_CALLBACK = 1  /* user operator: hconv_desc.mult_fn / mult_user, any A >= 1, B >= 1 */
+} hconv_mult;
+
+/* User multiplication operator (SPEC.md:396-399 MultOperator{A, B, apply}; PAPER.md:215,254
+ * "F_b <- mult(F_a)").  Called once per residue block of the innermost axis (per batch chunk)
+ * with the transformed blocks of the A inputs in F[0..A) and must leave the B outputs in
+ * F[0..B), in place; F has max(A, B) entries, each `count` values.  Pointwise:
+ * output element k depends only on the inputs' element k, and every F[i] uses the same element
+ * order, which is otherwise the library's choice.  Values are complex128 (complex / centered
+ * innermost axis) or float64 (real != 0: a Hermitian axis' transformed residues are real,
+ * PAPER.md:484-485).
+ * CUDA library: device pointers; enqueue the work on `stream` (a cudaStream_t) and return
+ * without synchronising.  Oracle: host pointers, stream NULL.  Return 0 on success; any other
+ * value aborts the convolution with HCONV_INVALID_ARG.                                      */
+typedef int (*hconv_mult_fn)(void* const* F, size_t A, size_t B, size_t count, int real, void* user, void* stream);
 
 /* plan.hpp:39-62 PlanParams (field for field; kind = {symmetry, regime}) */
 typedef struct hconv_params {
@@ -107,6 +123,8 @@ typedef struct hconv_desc {
   size_t dist;           /* 1D: elements between copies; 0 = stored length */
   int device;            /* CUDA ordinal (ignored by the oracle) */
   int flags;             /* reserved, 0 */
+  hconv_mult_fn mult_fn; /* HCONV_MULT_CALLBACK: the operator (else ignored) */
+  void* mult_user;       /* passed through to mult_fn */
 } hconv_desc;
 
 typedef struct hconv_plan hconv_plan;
@@ -117,6 +135,8 @@ hconv_status hconv_plan_params(const hconv_plan* plan, int axis, hconv_params* o
 size_t hconv_plan_workspace_bytes(const hconv_plan* plan);
 /* in[A], out[B]: complex128 arrays with the stored layout of the descriptor.
  * out[b] == in[b] (in place, the reference's convention, Alg. convolve) is allowed.
+ * A == 2, B == 1 with the built-in product runs the fused kernels; other operators run the
+ * residue loop through work blocks (A forward padded FFTs, mult, B backward padded FFTs).
  * CUDA library: device pointers, asynchronous on stream (cudaStream_t, NULL = legacy).
  * Oracle: host pointers, stream ignored.                                           */
 hconv_status hconv_convolve(hconv_plan* plan, const void* const* in, void* const* out, void* stream);

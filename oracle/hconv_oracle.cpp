@@ -476,26 +476,62 @@ static void forward_conjugate_pair(const Params& P, const cd* f, size_t v, cd* F
 }
 
 // ------------------------------------------------------------- drivers ------
-// Alg. convolve / convolveX with mult = builtin product.
-// inputs[a]: stored-length sequences; output written to out (stored length).
-static void conv1d(const Params& P, size_t A, const cd* const* in, cd* out) {
-  const size_t bl = block_len(P), Ls = stored_len(P), qm = P.q * P.m;
-  std::vector<cd> h(Ls, 0.0), Fa(bl), Fp(bl), V(Ls);
-  for (size_t r = 0; r < P.n; ++r) {
-    for (size_t a = 0; a < A; ++a) {
-      forward(P, in[a], r, a == 0 ? Fp.data() : Fa.data());
-      if (a > 0) {
-        if (P.sym == HCONV_HERMITIAN)
-          for (size_t i = 0; i < bl; ++i) Fp[i] = cd(Fp[i].real() * Fa[i].real(), 0.0);
-        else
-          for (size_t i = 0; i < bl; ++i) Fp[i] *= Fa[i];
-      }
+// MultOperator: builtin_mult_product(A) or a user callback
+// (include/hconv.h hconv_mult_fn), applied in place to the max(A, B) transformed blocks F[i] of
+// one residue.  Hermitian residues are real: the callback
+// sees float64 values.
+struct Mult {
+  size_t A = 2, B = 1;
+  int kind = HCONV_MULT_PRODUCT;
+  hconv_mult_fn fn = nullptr;
+  void* user = nullptr;
+  size_t W() const { return std::max(A, B); }
+};
+static void apply_mult(const Mult& mu, bool real, std::vector<std::vector<cd>>& F, size_t bl) {
+  if (mu.kind == HCONV_MULT_PRODUCT) {
+    for (size_t a = 1; a < mu.A; ++a) {
+      if (real)
+        for (size_t i = 0; i < bl; ++i) F[0][i] = cd(F[0][i].real() * F[a][i].real(), 0.0);
+      else
+        for (size_t i = 0; i < bl; ++i) F[0][i] *= F[a][i];
     }
-    backward(P, Fp.data(), r, V.data());
-    for (size_t j = 0; j < Ls; ++j) h[j] += V[j];
+    return;
+  }
+  std::vector<void*> ptrs(mu.W());
+  std::vector<std::vector<double>> R;
+  if (real) {
+    R.assign(mu.W(), std::vector<double>(bl, 0.0));
+    for (size_t a = 0; a < mu.A; ++a)
+      for (size_t i = 0; i < bl; ++i) R[a][i] = F[a][i].real();
+    for (size_t w = 0; w < mu.W(); ++w) ptrs[w] = R[w].data();
+  } else {
+    for (size_t w = 0; w < mu.W(); ++w) ptrs[w] = F[w].data();
+  }
+  const int rc = mu.fn(ptrs.data(), mu.A, mu.B, bl, real ? 1 : 0, mu.user, nullptr);
+  if (rc != 0) throw std::invalid_argument("multiplication operator callback returned " + std::to_string(rc));
+  if (real)
+    for (size_t b = 0; b < mu.B; ++b)
+      for (size_t i = 0; i < bl; ++i) F[b][i] = cd(R[b][i], 0.0);
+}
+
+// Alg. convolve / convolveX: the A forward transforms of each residue,
+// mult, the B backward transforms accumulated into h_b, then f_b <- h_b / (qm).
+// in[a]: stored-length sequences; out[b] (stored length) may alias in[b].
+static void conv1d(const Params& P, const Mult& mu, const cd* const* in, cd* const* out) {
+  const size_t bl = block_len(P), Ls = stored_len(P), qm = P.q * P.m;
+  std::vector<std::vector<cd>> h(mu.B, std::vector<cd>(Ls, 0.0)), F(mu.W(), std::vector<cd>(bl));
+  std::vector<cd> V(Ls);
+  for (size_t r = 0; r < P.n; ++r) {
+    for (size_t a = 0; a < mu.A; ++a) forward(P, in[a], r, F[a].data());
+    apply_mult(mu, P.sym == HCONV_HERMITIAN, F, bl);
+    for (size_t b = 0; b < mu.B; ++b) {
+      backward(P, F[b].data(), r, V.data());
+      for (size_t j = 0; j < Ls; ++j) h[b][j] += V[j];
+    }
   }
   const double s = 1.0 / (double)qm;
-  for (size_t j = 0; j < Ls; ++j) out[j] = h[j] * s;
+  for (size_t b = 0; b < mu.B; ++b)
+    for (size_t j = 0; j < Ls; ++j) out[b][j] = h[b][j] * s;
 }
 
 struct AxisP {
@@ -506,17 +542,17 @@ struct AxisP {
 // convolve_nd: for each outer residue, forward the outer axis on every
 // inner column, convolve each spectral line recursively, inverse the outer axis and accumulate.
 // arrays are row-major with extents stored[level..d-1].
-static void convnd_rec(const std::vector<AxisP>& ax, size_t level, size_t A, const std::vector<const cd*>& in,
-                       cd* out, bool parallel) {
-  const size_t d = ax.size();
-  if (level == d - 1) { conv1d(ax[level].P, A, in.data(), out); return; }
+static void convnd_rec(const std::vector<AxisP>& ax, size_t level, const Mult& mu, const std::vector<const cd*>& in,
+                       const std::vector<cd*>& out, bool parallel) {
+  const size_t d = ax.size(), A = mu.A, Bo = mu.B;
+  if (level == d - 1) { conv1d(ax[level].P, mu, in.data(), out.data()); return; }
   const Params& P = ax[level].P;
   const size_t Lx = ax[level].stored, bl = block_len(P), qm = P.q * P.m;
   size_t inner = 1;
   for (size_t k = level + 1; k < d; ++k) inner *= ax[k].stored;
-  std::vector<cd> h(Lx * inner, 0.0);
+  std::vector<std::vector<cd>> h(Bo, std::vector<cd>(Lx * inner, 0.0));
   std::vector<std::vector<cd>> F(A, std::vector<cd>(bl * inner));
-  std::vector<cd> R(bl * inner);
+  std::vector<std::vector<cd>> R(Bo, std::vector<cd>(bl * inner));
   for (size_t r = 0; r < P.n; ++r) {
     for (size_t a = 0; a < A; ++a) {
 #pragma omp parallel for schedule(dynamic, 16) if (parallel)
@@ -530,19 +566,24 @@ static void convnd_rec(const std::vector<AxisP>& ax, size_t level, size_t A, con
 #pragma omp parallel for schedule(dynamic, 1) if (parallel)
     for (size_t l = 0; l < bl; ++l) {
       std::vector<const cd*> sub(A);
+      std::vector<cd*> subo(Bo);
       for (size_t a = 0; a < A; ++a) sub[a] = F[a].data() + l * inner;
-      convnd_rec(ax, level + 1, A, sub, R.data() + l * inner, false);
+      for (size_t b = 0; b < Bo; ++b) subo[b] = R[b].data() + l * inner;
+      convnd_rec(ax, level + 1, mu, sub, subo, false);
     }
+    for (size_t b = 0; b < Bo; ++b) {
 #pragma omp parallel for schedule(dynamic, 16) if (parallel)
-    for (size_t c = 0; c < inner; ++c) {
-      std::vector<cd> Fc(bl), V(Lx);
-      for (size_t l = 0; l < bl; ++l) Fc[l] = R[l * inner + c];
-      backward(P, Fc.data(), r, V.data());
-      for (size_t x = 0; x < Lx; ++x) h[x * inner + c] += V[x];
+      for (size_t c = 0; c < inner; ++c) {
+        std::vector<cd> Fc(bl), V(Lx);
+        for (size_t l = 0; l < bl; ++l) Fc[l] = R[b][l * inner + c];
+        backward(P, Fc.data(), r, V.data());
+        for (size_t x = 0; x < Lx; ++x) h[b][x * inner + c] += V[x];
+      }
     }
   }
   const double s = 1.0 / (double)qm;
-  for (size_t i = 0; i < Lx * inner; ++i) out[i] = h[i] * s;
+  for (size_t b = 0; b < Bo; ++b)
+    for (size_t i = 0; i < Lx * inner; ++i) out[b][i] = h[b][i] * s;
 }
 
 // ---------------------------------------------------- brute-force oracles ---
@@ -814,8 +855,14 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
   return guarded([&] {
     if (!desc || !out) throw std::invalid_argument("null argument");
     if (desc->dims < 1 || desc->dims > 3) throw std::invalid_argument("dims must be 1, 2 or 3");
-    if (desc->mult != HCONV_MULT_PRODUCT) throw std::invalid_argument("unknown multiplication operator");
-    if (desc->A < 2 || desc->B != 1) throw std::invalid_argument("builtin product requires A >= 2, B == 1");
+    if (desc->mult == HCONV_MULT_PRODUCT) {
+      if (desc->A < 2 || desc->B != 1) throw std::invalid_argument("builtin_mult_product needs A >= 2 and B == 1");
+    } else if (desc->mult == HCONV_MULT_CALLBACK) {
+      if (!desc->mult_fn) throw std::invalid_argument("HCONV_MULT_CALLBACK without mult_fn");
+      if (desc->A < 1 || desc->B < 1) throw std::invalid_argument("multiplication operator arity: A >= 1, B >= 1");
+    } else {
+      throw std::invalid_argument("unknown multiplication operator");
+    }
     auto* p = new hconv_plan();
     p->d = *desc;
     const bool herm = desc->axis[desc->dims - 1].symmetry == HCONV_HERMITIAN;
@@ -840,26 +887,45 @@ hconv_status hconv_plan_params(const hconv_plan* p, int axis, hconv_params* o) {
 size_t hconv_plan_workspace_bytes(const hconv_plan*) { return 0; }
 hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* out, void* /*stream*/) {
   return guarded([&] {
-    if (!p) throw std::invalid_argument("null plan");
-    const size_t A = p->d.A;
+    if (!p || !in || !out) throw std::invalid_argument("null argument");
+    Mult mu;
+    mu.A = p->d.A; mu.B = p->d.B; mu.kind = p->d.mult; mu.fn = p->d.mult_fn; mu.user = p->d.mult_user;
+    const size_t A = mu.A, Bo = mu.B;
+    for (size_t a = 0; a < A; ++a) if (!in[a]) throw std::invalid_argument("null input array");
+    for (size_t b = 0; b < Bo; ++b) if (!out[b]) throw std::invalid_argument("null output array");
+    // a user callback is not assumed thread-safe: the oracle calls it from one thread
+    const bool par = mu.kind == HCONV_MULT_PRODUCT;
     if (p->d.dims == 1) {
       const size_t Ls = p->ax[0].stored, dist = p->d.dist ? p->d.dist : Ls, C = p->d.C ? p->d.C : 1;
-      std::vector<cd> res(C * Ls);
-#pragma omp parallel for schedule(dynamic, 1)
+      std::vector<std::vector<cd>> res(Bo, std::vector<cd>(C * Ls));
+      std::string err;
+#pragma omp parallel for schedule(dynamic, 1) if (par)
       for (size_t c = 0; c < C; ++c) {
         std::vector<const cd*> ins(A);
+        std::vector<cd*> outs(Bo);
         for (size_t a = 0; a < A; ++a) ins[a] = (const cd*)in[a] + c * dist;
-        conv1d(p->ax[0].P, A, ins.data(), res.data() + c * Ls);
+        for (size_t b = 0; b < Bo; ++b) outs[b] = res[b].data() + c * Ls;
+        try {
+          conv1d(p->ax[0].P, mu, ins.data(), outs.data());
+        } catch (const std::exception& e) {
+#pragma omp critical
+          err = e.what();
+        }
       }
-      for (size_t c = 0; c < C; ++c) std::copy(res.begin() + c * Ls, res.begin() + (c + 1) * Ls, (cd*)out[0] + c * dist);
+      if (!err.empty()) throw std::invalid_argument(err);
+      for (size_t b = 0; b < Bo; ++b)
+        for (size_t c = 0; c < C; ++c)
+          std::copy(res[b].begin() + c * Ls, res[b].begin() + (c + 1) * Ls, (cd*)out[b] + c * dist);
     } else {
       size_t tot = 1;
       for (auto& a : p->ax) tot *= a.stored;
       std::vector<const cd*> ins(A);
       for (size_t a = 0; a < A; ++a) ins[a] = (const cd*)in[a];
-      std::vector<cd> res(tot);
-      convnd_rec(p->ax, 0, A, ins, res.data(), true);
-      std::copy(res.begin(), res.end(), (cd*)out[0]);
+      std::vector<std::vector<cd>> res(Bo, std::vector<cd>(tot));
+      std::vector<cd*> outs(Bo);
+      for (size_t b = 0; b < Bo; ++b) outs[b] = res[b].data();
+      convnd_rec(p->ax, 0, mu, ins, outs, par);
+      for (size_t b = 0; b < Bo; ++b) std::copy(res[b].begin(), res[b].end(), (cd*)out[b]);
     }
   });
 }

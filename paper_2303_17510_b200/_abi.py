@@ -14,7 +14,11 @@ REPO = ROOT.parent
 OK, INVALID_ARG, UNSUPPORTED, CUDA_ERROR, NCCL_ERROR, ALLOC, INTERNAL = range(7)
 COMPLEX, CENTERED, HERMITIAN = 0, 1, 2
 P1, P2, INNER = 0, 1, 2
-MULT_PRODUCT = 0
+MULT_PRODUCT, MULT_CALLBACK = 0, 1
+
+# include/hconv.h hconv_mult_fn: (F, A, B, count, real, user, stream) -> int (0 = success)
+MultFn = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_void_p), C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.c_void_p,
+                     C.c_void_p)
 
 
 class Params(C.Structure):
@@ -42,6 +46,8 @@ class Desc(C.Structure):
         ("dist", C.c_size_t),
         ("device", C.c_int),
         ("flags", C.c_int),
+        ("mult_fn", C.c_void_p),
+        ("mult_user", C.c_void_p),
     ]
 
 

@@ -666,9 +666,10 @@ struct HostPipe {
   static constexpr int kSlots = 3;
   cudaStream_t st[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
   cudaEvent_t loaded[kSlots] = {}, done[kSlots] = {}, drained[kSlots] = {};
-  double2* buf[kSlots][2] = {};  // per slot: input 0 (also the output, in place) and input 1
-  size_t elems = 0;              // per buffer
-  int nslots = 0;                // slots allocated
+  std::vector<double2*> buf[kSlots];  // per slot: max(A, B) arrays (inputs, then outputs in place)
+  size_t elems = 0;                   // per buffer
+  int nslots = 0;                     // slots allocated
+  size_t width = 0;                   // buffers per slot
   bool ready = false;
   void init() {
     if (ready) return;
@@ -680,19 +681,23 @@ struct HostPipe {
     }
     ready = true;
   }
-  void ensure(size_t n, int slots) {
-    if (n <= elems && slots <= nslots) return;
-    for (auto& sl : buf)
-      for (auto& b : sl) {
+  void ensure(size_t n, int slots, size_t w) {
+    if (n <= elems && slots <= nslots && w <= width) return;
+    for (auto& sl : buf) {
+      for (auto& b : sl)
         if (b) CK(cudaFree(b));
-        b = nullptr;
-      }
+      sl.clear();
+    }
     elems = 0;
     nslots = 0;
-    for (int k = 0; k < slots; ++k)
+    width = 0;
+    for (int k = 0; k < slots; ++k) {
+      buf[k].assign(w, nullptr);
       for (auto& b : buf[k]) CK(cudaMalloc(&b, n * sizeof(double2)));
+    }
     elems = n;
     nslots = slots;
+    width = w;
   }
   ~HostPipe() {
     for (auto& sl : buf)
@@ -713,11 +718,17 @@ struct hconv_plan {
   int device = 0;
   std::vector<AxisPlan> ax;
   Scratch scratch;                    // conv1d accumulator slots
+  Scratch gwork, gacc;                // general operators: work blocks and accumulators
   std::vector<double2*> buffers;      // N-D work / accumulator buffers
   std::vector<long long> chunk;               // per level: arrays processed per pass (L2 blocking)
   PlanReport report;
   HostPipe host;                      // hconv_convolve_host
+  size_t W() const { return std::max(d.A, d.B); }
+  // the fused kernels compute the binary product; every other operator runs the general loop
+  bool fused() const { return d.mult == HCONV_MULT_PRODUCT && d.A == 2 && d.B == 1; }
   ~hconv_plan() {
+    gwork.release();
+    gacc.release();
     scratch.release();
     for (double2* b : buffers)
       if (b) cudaFree(b);
@@ -733,21 +744,105 @@ size_t inner_elems(const hconv_plan* P, int level) {
   return x;
 }
 
-// buffers layout: for level l < d-1: A work buffers then one accumulator
-double2* level_work(hconv_plan* P, int level, int a) { return P->buffers[level * (P->d.A + 1) + a]; }
-double2* level_acc(hconv_plan* P, int level) { return P->buffers[level * (P->d.A + 1) + P->d.A]; }
+// buffers layout: for level l < d-1: max(A, B) work buffers, then B accumulators
+double2* level_work(hconv_plan* P, int level, int a) { return P->buffers[level * (P->W() + P->d.B) + a]; }
+double2* level_acc(hconv_plan* P, int level, int b) { return P->buffers[level * (P->W() + P->d.B) + P->W() + b]; }
+
+// ------------------------------------------------- general multiplication operators ----
+// builtin_mult_product(A) for A != 2: F_0 <- F_0 F_1 ... F_{A-1}, pointwise
+constexpr size_t kMaxArity = 16;
+struct BlockPtrs {
+  void* p[kMaxArity];
+};
+__global__ void k_mult_product(BlockPtrs F, int A, long long count, int real) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (real) {
+      double acc = ((const double*)F.p[0])[i];
+      for (int a = 1; a < A; ++a) acc *= ((const double*)F.p[a])[i];
+      ((double*)F.p[0])[i] = acc;
+    } else {
+      double2 acc = ((const double2*)F.p[0])[i];
+      for (int a = 1; a < A; ++a) acc = hc::cmul(acc, ((const double2*)F.p[a])[i]);
+      ((double2*)F.p[0])[i] = acc;
+    }
+  }
+}
+
+// MultOperator.apply on one residue's transformed blocks, in place
+void apply_mult(const hconv_plan* P, double2* const* F, long long count, bool real, cudaStream_t s) {
+  if (P->d.mult == HCONV_MULT_PRODUCT) {
+    BlockPtrs b{};
+    for (size_t a = 0; a < P->d.A; ++a) b.p[a] = F[a];
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((count + 255) / 256, 8LL * dev_info().sms));
+    k_mult_product<<<blocks, 256, 0, s>>>(b, (int)P->d.A, count, real ? 1 : 0);
+    CK(cudaGetLastError());
+    return;
+  }
+  void* ptrs[kMaxArity];
+  for (size_t a = 0; a < P->W(); ++a) ptrs[a] = F[a];
+  const int rc = P->d.mult_fn(ptrs, P->d.A, P->d.B, (size_t)count, real ? 1 : 0, P->d.mult_user, s);
+  if (rc != 0) throw std::invalid_argument("multiplication operator callback returned " + std::to_string(rc));
+}
+
+// Alg. convolve / convolveX for a general operator over C lines of `dist`
+// elements: per chunk of lines and residue v, the A forward padded FFTs into work blocks
+// (natural block order), mult, and the B backward padded FFTs accumulated in separate buffers
+// (the last residue scales by 1/qm and writes out[b], which may alias an input: every input
+// line of the chunk has been transformed by then).  Chunks keep the work blocks L2-resident.
+void conv1d_general(hconv_plan* P, const AxisPlan& ap, long long C, long long dist, const double2* const* in,
+                    double2* const* out, cudaStream_t s) {
+  if (C == 0) return;
+  const size_t A = P->d.A, Bo = P->d.B, W = P->W();
+  const long long Bl = ap.dev.B, S = (long long)ap.data, n = ap.dev.n;
+  const bool real = ap.dev.sym == hc::SYM_HERMITIAN;
+  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 96.0;
+  const long long per_line = (long long)(W * Bl + (n > 1 ? Bo * dist : 0)) * (long long)sizeof(double2);
+  const long long chunk = std::max<long long>(1, std::min<long long>(C, (long long)(block_mb * 1048576.0 / per_line)));
+  const long long acc_elems = (chunk - 1) * dist + S;
+  P->gwork.ensure((size_t)(W * chunk * Bl) * sizeof(double2));
+  if (n > 1) P->gacc.ensure((size_t)(Bo * acc_elems) * sizeof(double2));
+  std::vector<double2*> work(W), acc(Bo, nullptr);
+  for (size_t w = 0; w < W; ++w) work[w] = P->gwork.p + w * chunk * Bl;
+  if (n > 1)
+    for (size_t b = 0; b < Bo; ++b) acc[b] = P->gacc.p + b * acc_elems;
+  const double scale = 1.0 / (double)ap.dev.qm;
+  for (long long c0 = 0; c0 < C; c0 += chunk) {
+    const long long cnt = std::min(chunk, C - c0);
+    const hc::Lines lin{cnt, 1, dist, 0, 1};  // data lines of the chunk
+    const hc::Lines wl{cnt, 1, Bl, 0, 1};     // work blocks (complex128, or float64 when real)
+    for (long long v = 0; v < n; ++v) {
+      for (size_t a = 0; a < A; ++a) launch_fwd(ap, lin, wl, in[a] + c0 * dist, work[a], (int)v, 0, s);
+      apply_mult(P, work.data(), cnt * Bl, real, s);
+      const bool first = v == 0, last = v == n - 1;
+      for (size_t b = 0; b < Bo; ++b)
+        launch_bwd(ap, wl, lin, work[b], last ? out[b] + c0 * dist : acc[b], first ? nullptr : acc[b],
+                   last ? scale : 1.0, (int)v, 0, s);
+    }
+  }
+}
+
+// 1D convolution of C lines: the fused kernel for the binary product, else the general loop
+void conv1d(hconv_plan* P, const AxisPlan& ap, long long C, long long dist, const double2* const* in,
+            double2* const* out, cudaStream_t s) {
+  if (P->fused()) {
+    const hc::Lines lin{C, 1, dist, 0, 1};
+    launch_conv(ap, lin, in[0], in[1], out[0], P->scratch, s);
+  } else {
+    conv1d_general(P, ap, C, dist, in, out, s);
+  }
+}
 
 // convolve_nd as grid-wide passes: for each outer residue v, forward the
 // outer axis of every column into work buffers, convolve the spectral lines recursively
 // (in place into work[0]), inverse the outer axis and accumulate (one normalisation per axis).
-void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, double2* out, cudaStream_t s) {
+void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, double2* const* out, cudaStream_t s) {
   const int d = (int)P->ax.size();
   const AxisPlan& ap = P->ax[level];
   const long long inner = (long long)inner_elems(P, level);
   const long long Lx = (long long)ap.data, asz = Lx * inner;
   if (level == d - 1) {
-    const hc::Lines lin{NB, 1, asz, 0, 1};
-    launch_conv(ap, lin, in[0], in[1], out, P->scratch, s);
+    conv1d(P, ap, NB, asz, in, out, s);
     return;
   }
   // L2 blocking: below the top level the NB arrays (spectral planes of the parent axis) are
@@ -757,21 +852,24 @@ void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, 
     const long long nb = std::min(chunk, NB - c0);
     std::vector<const double2*> inc(P->d.A);
     for (size_t a = 0; a < P->d.A; ++a) inc[a] = in[a] + c0 * asz;
-    double2* outc = out + c0 * asz;
     const long long B = ap.dev.B, n = ap.dev.n;
     const hc::Lines cols{nb * inner, inner, asz, 1, inner};       // columns of the input arrays
     const hc::Lines wcols{nb * inner, inner, B * inner, 1, inner};  // columns of the work arrays
-    double2* acc = level_acc(P, level);
     std::vector<const double2*> sub(P->d.A);
+    std::vector<double2*> subo(P->d.B);  // the subconvolutions write their B outputs in place
     for (size_t a = 0; a < P->d.A; ++a) sub[a] = level_work(P, level, (int)a);
+    for (size_t b = 0; b < P->d.B; ++b) subo[b] = level_work(P, level, (int)b);
     const double scale = 1.0 / (double)ap.dev.qm;
     for (int v = 0; v < n; ++v) {
       for (size_t a = 0; a < P->d.A; ++a) launch_fwd(ap, cols, wcols, inc[a], level_work(P, level, (int)a), v, 0, s);
-      nd_level(P, level + 1, nb * B, sub.data(), level_work(P, level, 0), s);
+      nd_level(P, level + 1, nb * B, sub.data(), subo.data(), s);
       const bool first = v == 0, last = v == n - 1;
-      double2* dst = last ? outc : acc;
-      const double2* accsrc = first ? nullptr : acc;
-      launch_bwd(ap, wcols, cols, level_work(P, level, 0), dst, accsrc, last ? scale : 1.0, v, 0, s);
+      for (size_t b = 0; b < P->d.B; ++b) {
+        double2* acc = level_acc(P, level, (int)b);
+        double2* dst = last ? out[b] + c0 * asz : acc;
+        const double2* accsrc = first ? nullptr : acc;
+        launch_bwd(ap, wcols, cols, level_work(P, level, (int)b), dst, accsrc, last ? scale : 1.0, v, 0, s);
+      }
     }
   }
 }
@@ -779,8 +877,16 @@ void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, 
 void check_desc(const hconv_desc* d) {
   if (!d) throw std::invalid_argument("null descriptor");
   if (d->dims < 1 || d->dims > 3) throw std::invalid_argument("dims must be 1, 2 or 3");
-  if (d->mult != HCONV_MULT_PRODUCT) throw std::invalid_argument("unknown multiplication operator");
-  if (d->A != 2 || d->B != 1) throw Unsupported("builtin product kernels are binary: A == 2, B == 1");
+  if (d->mult == HCONV_MULT_PRODUCT) {
+    // builtin_mult_product(A): B = 1, A >= 2
+    if (d->A < 2 || d->B != 1) throw std::invalid_argument("builtin_mult_product needs A >= 2 and B == 1");
+  } else if (d->mult == HCONV_MULT_CALLBACK) {
+    if (!d->mult_fn) throw std::invalid_argument("HCONV_MULT_CALLBACK without mult_fn");
+    if (d->A < 1 || d->B < 1) throw std::invalid_argument("multiplication operator arity: A >= 1, B >= 1");
+  } else {
+    throw std::invalid_argument("unknown multiplication operator");
+  }
+  if (std::max(d->A, d->B) > kMaxArity) throw Unsupported("operator arity above 16");
 }
 
 // Build the axis plans for chosen subtransform sizes and allocate the N-D work buffers.
@@ -803,19 +909,21 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
   long long NB = 1;
   for (int l = 0; l < d - 1; ++l) {
     const long long inner = (long long)inner_elems(P, l);
-    const long long per = (long long)(desc->A * P->ax[l].dev.B + P->ax[l].data) * inner * (long long)sizeof(double2);
+    const long long per = (long long)(P->W() * P->ax[l].dev.B + desc->B * P->ax[l].data) * inner * (long long)sizeof(double2);
     long long ch = NB;
     if (l > 0 && block_mb > 0) ch = std::max<long long>(1, std::min<long long>(NB, (long long)(block_mb * 1048576.0 / per)));
     P->chunk[l] = ch;
     const long long work = ch * P->ax[l].dev.B * inner, acc = ch * (long long)P->ax[l].data * inner;
-    for (size_t a = 0; a < desc->A; ++a) {
+    for (size_t a = 0; a < P->W(); ++a) {
       double2* b = nullptr;
       CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
       P->buffers.push_back(b);
     }
-    double2* b = nullptr;
-    CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
-    P->buffers.push_back(b);
+    for (size_t b_ = 0; b_ < desc->B; ++b_) {
+      double2* b = nullptr;
+      CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
+      P->buffers.push_back(b);
+    }
     NB = ch * P->ax[l].dev.B;
   }
 }
@@ -892,13 +1000,15 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
   if (total > 1) {
     size_t elems = 1;
     for (size_t x : data) elems *= x;
-    double2 *f = nullptr, *g = nullptr, *o = nullptr;
-    CK(cudaMalloc(&f, elems * sizeof(double2)));
-    CK(cudaMalloc(&g, elems * sizeof(double2)));
-    CK(cudaMalloc(&o, elems * sizeof(double2)));
-    k_fill_uniform<<<256, 256>>>(7, 0, 0, (long long)elems, f);
-    k_fill_uniform<<<256, 256>>>(7, 1, 0, (long long)elems, g);
+    // A synthetic inputs and B outputs (the operator of the plan is the one timed)
+    std::vector<double2*> arrs(desc->A + desc->B, nullptr);
+    for (size_t i = 0; i < arrs.size(); ++i) {
+      CK(cudaMalloc(&arrs[i], elems * sizeof(double2)));
+      if (i < desc->A) k_fill_uniform<<<256, 256>>>(7, i, 0, (long long)elems, arrs[i]);
+    }
     CK(cudaGetLastError());
+    const double2* const* ins = arrs.data();
+    double2* const* outs = arrs.data() + desc->A;
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -911,12 +1021,11 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
         rem /= options[k].size();
       }
       build_plan(P, ms, syms);
-      const double2* ins[2] = {f, g};
-      nd_level(P, 0, 1, ins, o, 0);
+      nd_level(P, 0, 1, ins, outs, 0);
       double t = 1e30;
       for (int r = 0; r < 3; ++r) {
         CK(cudaEventRecord(e0));
-        nd_level(P, 0, 1, ins, o, 0);
+        nd_level(P, 0, 1, ins, outs, 0);
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float x = 0;
@@ -935,9 +1044,7 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaFree(f);
-    cudaFree(g);
-    cudaFree(o);
+    for (double2* a : arrs) cudaFree(a);
   }
   std::lock_guard<std::mutex> lk(cache.mu);
   for (int k = 0; k < d; ++k) cache.store(key + "|axis" + std::to_string(k), best[k], 0.0);
@@ -1087,36 +1194,53 @@ size_t hconv_plan_workspace_bytes(const hconv_plan* p) {
   for (int l = 0; l + 1 < d; ++l) {
     size_t inner = 1;
     for (int k = l + 1; k < d; ++k) inner *= p->ax[k].data;
-    b += (size_t)p->chunk[l] * (p->ax[l].dev.B * p->d.A + p->ax[l].data) * inner * sizeof(double2);
+    b += (size_t)p->chunk[l] * (p->ax[l].dev.B * p->W() + p->ax[l].data * p->d.B) * inner * sizeof(double2);
   }
-  return b;
+  return b + p->gwork.bytes + p->gacc.bytes;
+}
+
+// in[A] / out[B] pointer arrays of a call, null-checked
+static void io_arrays(const hconv_plan* p, const void* const* in, void* const* out, std::vector<const double2*>& ins,
+                      std::vector<double2*>& outs) {
+  if (!p || !in || !out) throw std::invalid_argument("null argument");
+  for (size_t a = 0; a < p->d.A; ++a) {
+    if (!in[a]) throw std::invalid_argument("null input array");
+    ins.push_back((const double2*)in[a]);
+  }
+  for (size_t b = 0; b < p->d.B; ++b) {
+    if (!out[b]) throw std::invalid_argument("null output array");
+    outs.push_back((double2*)out[b]);
+  }
 }
 
 hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* out, void* stream) {
   return guarded([&] {
-    if (!p || !in || !out || !in[0] || !in[1] || !out[0]) throw std::invalid_argument("null argument");
+    std::vector<const double2*> ins;
+    std::vector<double2*> outs;
+    io_arrays(p, in, out, ins, outs);
     CK(cudaSetDevice(p->device));
     cudaStream_t s = (cudaStream_t)stream;
-    const double2* ins[2] = {(const double2*)in[0], (const double2*)in[1]};
     if (p->d.dims == 1) {
       const AxisPlan& ap = p->ax[0];
       const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
-      const hc::Lines lin{(long long)(p->d.C ? p->d.C : 1), 1, dist, 0, 1};
-      launch_conv(ap, lin, ins[0], ins[1], (double2*)out[0], p->scratch, s);
+      conv1d(p, ap, (long long)(p->d.C ? p->d.C : 1), dist, ins.data(), outs.data(), s);
     } else {
-      nd_level(p, 0, 1, ins, (double2*)out[0], s);
+      nd_level(p, 0, 1, ins.data(), outs.data(), s);
     }
   });
 }
 
 hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* const* out) {
   return guarded([&] {
-    if (!p || !in || !out || !in[0] || !in[1] || !out[0]) throw std::invalid_argument("null argument");
+    std::vector<const double2*> hin_;
+    std::vector<double2*> hout_;
+    io_arrays(p, in, out, hin_, hout_);
     CK(cudaSetDevice(p->device));
     HostPipe& hp = p->host;
     hp.init();
-    const char* hin[2] = {(const char*)in[0], (const char*)in[1]};
-    char* hout = (char*)out[0];
+    const size_t A = p->d.A, Bo = p->d.B, W = p->W();
+    auto hin = [&](size_t a) { return (const char*)hin_[a]; };
+    auto hout = [&](size_t b) { return (char*)hout_[b]; };
     if (p->d.dims == 1) {
       const AxisPlan& ap = p->ax[0];
       const long long C = (long long)(p->d.C ? p->d.C : 1), S = (long long)ap.data;
@@ -1124,35 +1248,33 @@ hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* con
       const long long want = std::getenv("HCONV_HOST_CHUNKS") ? std::atoll(std::getenv("HCONV_HOST_CHUNKS")) : 8;
       const long long nch = std::max<long long>(1, std::min<long long>(C, want));
       const long long per = (C + nch - 1) / nch;
-      hp.ensure((size_t)((per - 1) * dist + S), (int)std::min<long long>(nch, HostPipe::kSlots));
+      hp.ensure((size_t)((per - 1) * dist + S), (int)std::min<long long>(nch, HostPipe::kSlots), W);
       int slot = 0;
       for (long long c0 = 0; c0 < C; c0 += per, slot = (slot + 1) % HostPipe::kSlots) {
         const long long cnt = std::min(per, C - c0);
         const size_t bytes = (size_t)((cnt - 1) * dist + S) * sizeof(double2);
         const size_t off = (size_t)(c0 * dist) * sizeof(double2);
-        double2* const* b = hp.buf[slot];
+        double2* const* b = hp.buf[slot].data();
         // slot reuse: its previous chunk has been copied back
         CK(cudaStreamWaitEvent(hp.st[0], hp.drained[slot], 0));
-        for (int a = 0; a < 2; ++a) CK(cudaMemcpyAsync(b[a], hin[a] + off, bytes, cudaMemcpyHostToDevice, hp.st[0]));
+        for (size_t a = 0; a < A; ++a) CK(cudaMemcpyAsync(b[a], hin(a) + off, bytes, cudaMemcpyHostToDevice, hp.st[0]));
         CK(cudaEventRecord(hp.loaded[slot], hp.st[0]));
         CK(cudaStreamWaitEvent(hp.st[1], hp.loaded[slot], 0));
-        const hc::Lines lin{cnt, 1, dist, 0, 1};
-        launch_conv(ap, lin, b[0], b[1], b[0], p->scratch, hp.st[1]);
+        conv1d(p, ap, cnt, dist, b, b, hp.st[1]);  // in place: outputs in the first B buffers
         CK(cudaEventRecord(hp.done[slot], hp.st[1]));
         CK(cudaStreamWaitEvent(hp.st[2], hp.done[slot], 0));
-        CK(cudaMemcpyAsync(hout + off, b[0], bytes, cudaMemcpyDeviceToHost, hp.st[2]));
+        for (size_t o = 0; o < Bo; ++o) CK(cudaMemcpyAsync(hout(o) + off, b[o], bytes, cudaMemcpyDeviceToHost, hp.st[2]));
         CK(cudaEventRecord(hp.drained[slot], hp.st[2]));
       }
       CK(cudaStreamSynchronize(hp.st[2]));
     } else {
       size_t n = 1;
       for (const AxisPlan& ap : p->ax) n *= ap.data;
-      hp.ensure(n, 1);
-      double2* const* b = hp.buf[0];
-      for (int a = 0; a < 2; ++a) CK(cudaMemcpyAsync(b[a], hin[a], n * sizeof(double2), cudaMemcpyHostToDevice, hp.st[1]));
-      const double2* ins[2] = {b[0], b[1]};
-      nd_level(p, 0, 1, ins, b[0], hp.st[1]);
-      CK(cudaMemcpyAsync(hout, b[0], n * sizeof(double2), cudaMemcpyDeviceToHost, hp.st[1]));
+      hp.ensure(n, 1, W);
+      double2* const* b = hp.buf[0].data();
+      for (size_t a = 0; a < A; ++a) CK(cudaMemcpyAsync(b[a], hin(a), n * sizeof(double2), cudaMemcpyHostToDevice, hp.st[1]));
+      nd_level(p, 0, 1, b, b, hp.st[1]);
+      for (size_t o = 0; o < Bo; ++o) CK(cudaMemcpyAsync(hout(o), b[o], n * sizeof(double2), cudaMemcpyDeviceToHost, hp.st[1]));
       CK(cudaStreamSynchronize(hp.st[1]));
     }
   });

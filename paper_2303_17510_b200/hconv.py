@@ -25,7 +25,7 @@ import enum
 import math
 import threading
 from dataclasses import dataclass, field
-from typing import Optional, Sequence
+from typing import Callable, Optional, Sequence, Union
 
 import torch
 
@@ -214,13 +214,57 @@ def backward(F: torch.Tensor, params: PlanParams, r: int, h: Optional[torch.Tens
 
 
 # ---------------------------------------------------------------- convolutions -------
+class _CudaArray:
+    """__cuda_array_interface__ view of a raw device pointer (no copy)."""
+
+    def __init__(self, ptr: int, count: int, real: bool):
+        self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8" if real else "<c16",
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
 @dataclass(frozen=True)
 class MultOperator:
-    """pointwise map of A transformed inputs to B outputs."""
+    """SPEC.md:396-399 MultOperator{A, B, apply}: pointwise map of A transformed inputs to B outputs.
+
+    kind MULT_PRODUCT is builtin_mult_product(A) (fused kernels for A = 2).  Otherwise the
+    operator is ``apply(blocks, real)``: ``blocks`` are max(A, B) device tensors of one residue
+    (complex128, or float64 for a Hermitian innermost axis, whose transformed residues are real,
+    PAPER.md:484-485); the A inputs are in blocks[:A] and the B outputs must be left in
+    blocks[:B], in place ("F_b <- mult(F_a)").  It runs on the library's stream
+    (torch's current stream inside the call).  ``fn`` instead takes the address of a native
+    ``hconv_mult_fn`` (include/hconv.h), e.g. a function of the caller's own CUDA library.
+    """
 
     A: int
     B: int
     kind: int = _abi.MULT_PRODUCT
+    apply: Optional[Callable] = None
+    fn: Optional[int] = None
+
+    def _native(self):
+        """(hconv_mult_fn address, keep-alive object) for the descriptor."""
+        if self.kind == _abi.MULT_PRODUCT:
+            return None, None
+        if self.fn is not None:
+            return self.fn, None
+        apply = self.apply
+
+        def _fn(F, A, B, count, real, user, stream):
+            try:
+                dev = torch.cuda.current_device()
+                blocks = [torch.as_tensor(_CudaArray(F[i], count, bool(real)), device=f"cuda:{dev}")
+                          for i in range(max(A, B))]
+                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+                    apply(blocks, bool(real))
+                return 0
+            except Exception:  # noqa: BLE001 -- the library turns a nonzero return into a status
+                import traceback
+
+                traceback.print_exc()
+                return 1
+
+        cb = _abi.MultFn(_fn)
+        return C.cast(cb, C.c_void_p).value, cb
 
 
 def builtin_mult_product(A: int = 2) -> MultOperator:
@@ -230,8 +274,17 @@ def builtin_mult_product(A: int = 2) -> MultOperator:
     return MultOperator(A, 1, _abi.MULT_PRODUCT)
 
 
+def mult_operator(A: int, B: int, apply: Callable) -> MultOperator:
+    """A general A -> B pointwise operator (see MultOperator)."""
+    if A < 1 or B < 1:
+        raise ValueError("multiplication operator arity: A >= 1, B >= 1")
+    return MultOperator(A, B, _abi.MULT_CALLBACK, apply=apply)
+
+
 class _Plan:
-    def __init__(self, desc: _abi.Desc):
+    def __init__(self, desc: _abi.Desc, mult: "MultOperator"):
+        fn, self._keep = mult._native()  # the callback must outlive the plan
+        desc.mult_fn = fn
         h = C.c_void_p()
         _check(lib().hconv_plan_create(C.byref(desc), C.byref(h)))
         self._h = h
@@ -262,15 +315,15 @@ class _Plan:
     def workspace_bytes(self) -> int:
         return lib().hconv_plan_workspace_bytes(self._h)
 
-    def _run(self, inputs: Sequence[torch.Tensor], out: torch.Tensor, stream) -> None:
+    def _run(self, inputs: Sequence[torch.Tensor], outs: Sequence[torch.Tensor], stream) -> None:
         ins = (C.c_void_p * len(inputs))(*[t.data_ptr() for t in inputs])
-        outs = (C.c_void_p * 1)(out.data_ptr())
-        _check(lib().hconv_convolve(self._h, ins, outs, _stream(stream)))
+        o = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+        _check(lib().hconv_convolve(self._h, ins, o, _stream(stream)))
 
-    def _run_host(self, inputs: Sequence[torch.Tensor], out: torch.Tensor) -> None:
+    def _run_host(self, inputs: Sequence[torch.Tensor], outs: Sequence[torch.Tensor]) -> None:
         ins = (C.c_void_p * len(inputs))(*[t.data_ptr() for t in inputs])
-        outs = (C.c_void_p * 1)(out.data_ptr())
-        _check(lib().hconv_convolve_host(self._h, ins, outs))
+        o = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+        _check(lib().hconv_convolve_host(self._h, ins, o))
 
 
 class Conv1dPlan(_Plan):
@@ -287,7 +340,7 @@ class Conv1dPlan(_Plan):
         d.dims = 1
         d.axis[0] = _abi.Axis(L, M, m or 0, int(symmetry))
         d.A, d.B, d.mult, d.C, d.dist, d.device = mult.A, mult.B, mult.kind, C_, dist, device
-        super().__init__(d)
+        super().__init__(d, mult)
         self.mult = mult
         self.params = self.axis_params(0)
 
@@ -315,7 +368,7 @@ class ConvPlanND(_Plan):
         for k, a in enumerate(axes):
             d.axis[k] = _abi.Axis(a.L, a.M, a.m or 0, int(a.symmetry))
         d.A, d.B, d.mult, d.C, d.dist, d.device = mult.A, mult.B, mult.kind, 1, 0, device
-        super().__init__(d)
+        super().__init__(d, mult)
         self.mult = mult
         self.axes = list(axes)
         self.params = [self.axis_params(k) for k in range(len(axes))]
@@ -329,34 +382,49 @@ def _check_mult(inputs, mult: MultOperator, plan: _Plan):
         raise ValueError("arity mismatch between inputs, mult and plan (SPEC.md:410)")
 
 
-def convolve(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: Conv1dPlan, out: Optional[torch.Tensor] = None,
+Outs = Optional[Union[torch.Tensor, Sequence[torch.Tensor]]]
+
+
+def _outs(out: Outs, ins: Sequence[torch.Tensor], B: int, conv) -> list[torch.Tensor]:
+    """B output arrays: by default the first B inputs (overwritten in place)."""
+    if out is None:
+        if B > len(ins):
+            raise ValueError("B > A: pass the B output arrays explicitly")
+        return list(ins[:B])
+    outs = [out] if isinstance(out, torch.Tensor) else list(out)
+    if len(outs) != B:
+        raise ValueError(f"expected {B} output arrays")
+    return [conv(o) for o in outs]
+
+
+def convolve(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: Conv1dPlan, out: Outs = None,
              stream=None) -> list[torch.Tensor]:
-    """Alg. convolve / convolveX: returns [h]; by default the result
-    overwrites inputs[0] (the reference's in-place convention)."""
+    """Alg. convolve / convolveX: returns the B outputs [h_0 .. h_{B-1}]; by
+    default they overwrite the first B inputs (the reference's in-place convention)."""
     _check_mult(inputs, mult, plan)
     ins = [_dev(t) for t in inputs]
     rows = plan.desc.C
     need = (rows - 1) * (plan.desc.dist or plan.params.dataLength()) + plan.params.dataLength()
-    for t in ins:
+    outs = _outs(out, ins, mult.B, _dev)
+    for t in ins + outs:
         if t.numel() < need:
-            raise ValueError("input smaller than the plan's C x dist layout")
-    o = ins[0] if out is None else _dev(out)
-    plan._run(ins, o, stream)
-    return [o]
+            raise ValueError("array smaller than the plan's C x dist layout")
+    plan._run(ins, outs, stream)
+    return outs
 
 
-def convolve_nd(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: ConvPlanND, out: Optional[torch.Tensor] = None,
+def convolve_nd(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: ConvPlanND, out: Outs = None,
                 stream=None) -> list[torch.Tensor]:
     """convolve_nd over contiguous arrays of shape plan.shape()."""
     _check_mult(inputs, mult, plan)
     shp = plan.shape()
     ins = [_dev(t) for t in inputs]
-    for t in ins:
+    outs = _outs(out, ins, mult.B, _dev)
+    for t in ins + outs:
         if tuple(t.shape) != shp:
             raise ValueError(f"expected shape {shp}, got {tuple(t.shape)}")
-    o = ins[0] if out is None else _dev(out)
-    plan._run(ins, o, stream)
-    return [o]
+    plan._run(ins, outs, stream)
+    return outs
 
 
 def _host(t: torch.Tensor) -> torch.Tensor:
@@ -366,26 +434,26 @@ def _host(t: torch.Tensor) -> torch.Tensor:
 
 
 def convolve_host(inputs: Sequence[torch.Tensor], mult: MultOperator, plan: "_Plan",
-                  out: Optional[torch.Tensor] = None) -> list[torch.Tensor]:
+                  out: Outs = None) -> list[torch.Tensor]:
     """convolve / convolve_nd on HOST tensors -- the reference library's calling convention
     (synchronous, host arrays).  The library streams a 1D batch through the device in chunks,
     overlapping host->device copies, the convolution and device->host copies (pin the tensors,
     ``t.pin_memory()``, for the overlap).  Computes on the GPU; there is no CPU path."""
     _check_mult(inputs, mult, plan)
     ins = [_host(t) for t in inputs]
+    outs = _outs(out, ins, mult.B, _host)
     if isinstance(plan, ConvPlanND):
         shp = plan.shape()
-        for t in ins:
+        for t in ins + outs:
             if tuple(t.shape) != shp:
                 raise ValueError(f"expected shape {shp}, got {tuple(t.shape)}")
     else:
         need = (plan.desc.C - 1) * (plan.desc.dist or plan.params.dataLength()) + plan.params.dataLength()
-        for t in ins:
+        for t in ins + outs:
             if t.numel() < need:
-                raise ValueError("input smaller than the plan's C x dist layout")
-    o = ins[0] if out is None else _host(out)
-    plan._run_host(ins, o)
-    return [o]
+                raise ValueError("array smaller than the plan's C x dist layout")
+    plan._run_host(ins, outs)
+    return outs
 
 
 def hermitian_symmetrize_boundary(f: torch.Tensor, Ls: Sequence[int]) -> torch.Tensor:

@@ -137,6 +137,43 @@ class Oracle:
             self.lib.hconv_plan_destroy(h)
         return out
 
+    def convolve_general(self, axes, inputs, B=1, apply=None, C_=1, dist=0):
+        """hconv_convolve with A = len(inputs) inputs and B outputs.  apply=None: builtin
+        product (B must be 1); else apply(blocks, real) is the operator on numpy views of the
+        max(A, B) transformed blocks (complex128, or float64 when real), in place."""
+        A = len(inputs)
+        d = _abi.Desc()
+        d.dims = len(axes)
+        for k, (L, M, m, s) in enumerate(axes):
+            d.axis[k] = _abi.Axis(L, M, m, s)
+        d.A, d.B, d.C, d.dist = A, B, C_, dist
+        cb = None
+        if apply is None:
+            d.mult = _abi.MULT_PRODUCT
+        else:
+            def _fn(F, A_, B_, count, real, user, stream):
+                try:
+                    dt = np.float64 if real else np.complex128
+                    blocks = [np.ctypeslib.as_array(C.cast(F[i], C.POINTER(C.c_double)), (count * (1 if real else 2),)).view(dt)
+                              for i in range(max(A_, B_))]
+                    apply(blocks, bool(real))
+                    return 0
+                except Exception:  # noqa: BLE001 -- reported as a status by the library
+                    return 1
+            cb = _abi.MultFn(_fn)
+            d.mult = _abi.MULT_CALLBACK
+            d.mult_fn = C.cast(cb, C.c_void_p)
+        h = C.c_void_p()
+        _abi.check(self.lib, self.lib.hconv_plan_create(C.byref(d), C.byref(h)))
+        ins = [np.ascontiguousarray(x, dtype=np.complex128) for x in inputs]
+        outs = [np.zeros_like(ins[0]) for _ in range(B)]
+        try:
+            _abi.check(self.lib, self.lib.hconv_convolve(h, (C.c_void_p * A)(*[x.ctypes.data for x in ins]),
+                                                         (C.c_void_p * B)(*[o.ctypes.data for o in outs]), None))
+        finally:
+            self.lib.hconv_plan_destroy(h)
+        return outs
+
     def direct(self, syms, Ls, f, g):
         f = np.ascontiguousarray(f, dtype=np.complex128)
         g = np.ascontiguousarray(g, dtype=np.complex128)
