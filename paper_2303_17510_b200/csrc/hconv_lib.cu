@@ -431,9 +431,32 @@ int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items
   return (int)std::max<long long>(1, std::min(need, (long long)nb * dev_info().sms));
 }
 
+// Pipelined column tiles (k_pfft_*_cols_pp): two tile buffers of gc x max(xs, rows) values plus
+// at least the middle-pass tables must fit; returns the staged table prefix (0 = does not fit).
+int cols_pp_tabn(const AxisPlan& ap, int rows, size_t* smem) {
+  static const bool off = std::getenv("HCONV_NO_COLS_PP") && std::getenv("HCONV_NO_COLS_PP")[0] == '1';
+  if (off || !ap.k->fwdcp) return 0;
+  const size_t bufs = 2 * (size_t)ap.k->gc * (size_t)std::max(ap.k->xs, rows);
+  if ((bufs + (size_t)ap.k->mt) * sizeof(double2) > kSmemCap) return 0;
+  const size_t room = kSmemCap / sizeof(double2) - bufs;
+  const int tabn = (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
+  *smem = (tabn + bufs) * sizeof(double2);
+  return tabn;
+}
+
 void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
                 int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  size_t smpp = 0;
+  int tpp = 0;
+  if (use_cols(ap, lin) && !ref_order && (tpp = cols_pp_tabn(ap, (int)ap.data, &smpp)) > 0) {
+    const int grid = grid_cols(ap.k->fwdcp_fn, ap.k, smpp, lin.count);
+    hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+    a.ax.tabn = tpp;
+    ap.k->fwdcp(a, grid, smpp, s);
+    CK(cudaGetLastError());
+    return;
+  }
   if (use_cols(ap, lin)) {
     const int tabn = cols_tabn(ap);
     const size_t sm = (size_t)(tabn + (size_t)ap.k->gc * ap.k->xs) * sizeof(double2);
@@ -456,6 +479,16 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
 void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
                 const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  size_t smpp = 0;
+  int tpp = 0;
+  if (use_cols(ap, lout) && !ref_order && (tpp = cols_pp_tabn(ap, ap.dev.Bc, &smpp)) > 0) {
+    const int grid = grid_cols(ap.k->bwdcp_fn, ap.k, smpp, lin.count);
+    hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+    a.ax.tabn = tpp;
+    ap.k->bwdcp(a, grid, smpp, s);
+    CK(cudaGetLastError());
+    return;
+  }
   if (use_cols(ap, lout)) {
     const int tabn = cols_tabn(ap);
     const size_t sm = (size_t)(tabn + (size_t)ap.k->gc * ap.k->xs) * sizeof(double2);

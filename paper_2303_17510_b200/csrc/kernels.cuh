@@ -930,6 +930,118 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
   }
 }
 
+// ------------------------------------------------- column-tile pfft, pipelined --
+// The same column tiles as k_pfft_fwd_cols / k_pfft_bwd_cols, software-pipelined: the CTA owns
+// two tile buffers of GC x max(XS, rows) values (element j of column g at [j GC + g]).  While
+// the FFT of tile k runs in one buffer (its staged input, then its exchanges), every thread's
+// cp.async copies gather tile k + gridDim.x into the other, so the strided row reads overlap
+// the butterflies instead of stalling them (the unpipelined kernels are ~40 % long-scoreboard
+// stalls at one CTA per SM).  Natural block order only (the N-D driver's work arrays).
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols_pp(FwdArgs p) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  const int rows = a.S;
+  const int bufn = GC * (rows > Cfg::XS ? rows : Cfg::XS);
+  double2* buf[2] = {smem + a.tabn, smem + a.tabn + bufn};
+  const long long ntiles = (p.lin.count + GC - 1) / GC;
+  const long long es = p.lin.es;
+  auto gather = [&](long long t, double2* B) HC_INL {
+    const long long item = t * GC + g;
+    if (t < ntiles && item < p.lin.count) {
+      const double2* src = p.f + p.lin.base(item);
+      for (int j = tid; j < rows; j += T) cp_async16(B + j * GC + g, src + j * es);
+    }
+    cp_async_commit();
+  };
+  gather(blockIdx.x, buf[0]);
+  int k = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    double2* X = buf[k & 1];
+    __syncthreads();  // the previous tile's exchanges in the other buffer are finished
+    gather(t + gridDim.x, buf[(k + 1) & 1]);
+    cp_async_wait<1>();
+    __syncthreads();  // tile t has landed (every thread's copies)
+    const long long item = t * GC + g;
+    const bool live = item < p.lin.count;
+    double2 v[Cfg::E];
+    if (live) load_pass0<SYM, Cfg>(v, a, tp, X + g, GC, p.v, tid);
+    __syncthreads();  // the staged tile is consumed before the first exchange overwrites it
+    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+    if (!live) continue;
+    const long long ob = p.lout.base(item), oes = p.lout.es;
+    double2* F = (double2*)p.F;
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { F[ob + (beta + (long long)RpL * Ki) * oes] = v[c * RL + Ki]; });
+    });
+  }
+  cp_async_wait<0>();
+}
+
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols_pp(BwdArgs p) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  constexpr int rows = Cfg::N;  // block values (complex)
+  constexpr int bufn = GC * Cfg::XS;
+  double2* buf[2] = {smem + a.tabn, smem + a.tabn + bufn};
+  const long long ntiles = (p.lin.count + GC - 1) / GC;
+  const long long ies = p.lin.es;
+  const double2* F = (const double2*)p.F;
+  auto gather = [&](long long t, double2* B) HC_INL {
+    const long long item = t * GC + g;
+    if (t < ntiles && item < p.lin.count) {
+      const double2* src = F + p.lin.base(item);
+      for (int j = tid; j < rows; j += T) cp_async16(B + j * GC + g, src + j * ies);
+    }
+    cp_async_commit();
+  };
+  gather(blockIdx.x, buf[0]);
+  int k = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    double2* X = buf[k & 1];
+    __syncthreads();
+    gather(t + gridDim.x, buf[(k + 1) & 1]);
+    cp_async_wait<1>();
+    __syncthreads();
+    const long long item = t * GC + g;
+    const bool live = item < p.lin.count;
+    double2 v[Cfg::E];
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { v[c * RL + Ki] = X[(beta + RpL * Ki) * GC + g]; });
+    });
+    __syncthreads();
+    fft_inverse<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+    if (!live) continue;
+    const long long ob = p.lout.base(item);
+    const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
+    store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
+  }
+  cp_async_wait<0>();
+}
+
 // ---------------------------------------------------------------- pfft fwd --
 template <int SYM, class Cfg, int G>
 __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {

@@ -30,6 +30,11 @@ struct KernelEntry {
   const void* bwdc_fn = nullptr;
   void (*fwdc)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   void (*bwdc)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  // pipelined column tiles (two tile buffers of GC x max(XS, rows) values)
+  const void* fwdcp_fn = nullptr;
+  const void* bwdcp_fn = nullptr;
+  void (*fwdcp)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  void (*bwdcp)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
 };
 
 // column groups per CTA: up to 8 adjacent columns (128 B rows), <= 1024 threads, and the
@@ -91,6 +96,14 @@ KernelEntry make_entry(const char* radix) {
     };
     e.bwdc = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
       k_pfft_bwd_cols<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+    };
+    e.fwdcp_fn = (const void*)k_pfft_fwd_cols_pp<SYM, Cfg, GC>;
+    e.bwdcp_fn = (const void*)k_pfft_bwd_cols_pp<SYM, Cfg, GC>;
+    e.fwdcp = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+      k_pfft_fwd_cols_pp<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+    };
+    e.bwdcp = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
+      k_pfft_bwd_cols_pp<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
     };
   }
   return e;

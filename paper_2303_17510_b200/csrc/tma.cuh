@@ -115,4 +115,17 @@ __device__ __forceinline__ void l2_prefetch(const void* src, uint32_t bytes) {
   }
 }
 
+// ---- per-thread asynchronous 16-byte global->shared copies (cp.async, LDGSTS) ----
+// Used where a tile is gathered from strided rows (column tiles of the N-D outer axes): each
+// thread copies its elements into the tile's shared-memory layout without staging them in
+// registers; completion per thread through commit/wait groups, then a CTA barrier.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 }  // namespace hc
