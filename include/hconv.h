@@ -22,6 +22,8 @@
  *   hconv_symmetry_from_name proj/include/hconv/plan.hpp:28   symmetryFromName
  *   hconv_pfft_forward       SPEC.md:158,176,194,258,276,331,349  forward1/2/Inner[C|H]
  *   hconv_pfft_backward      SPEC.md:167,185,203,267,285,340,358  backward1/2/Inner[C|H]
+ *   hconv_pfft_*_lines       the same over two-level strided line batches (PAPER.md:584-600
+ *                            outer-axis passes; used by the multi-GPU slab driver)
  *   hconv_plan_create        SPEC.md:400-403 Conv1dPlan, SPEC.md:469-472 ConvPlanND,
  *                            SPEC.md:533-550 tune_1d/tune_nd (when an axis has m == 0)
  *   hconv_convolve           SPEC.md:406-423 convolve/convolveC/convolveH,
@@ -106,6 +108,21 @@ hconv_status hconv_pfft_forward(const hconv_params* pp, const void* f, size_t di
 hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t residue, void* h, size_t dist,
                                  int accumulate, void* stream);
 
+/* Two-level line batches for the N-D and slab drivers (the strided outer-axis passes of
+ * PAPER.md:584-600): line l of a batch starts at element (l / nin) * d_out + (l % nin) * d_in
+ * and its values sit at element stride es (complex128 elements, or float64 for Hermitian
+ * blocks).  Blocks are in natural block order (the order the convolution kernels use, not the
+ * reference's F[u m + l]; pointwise operators do not see the difference).  Forward writes the
+ * block of residue `residue` of every line; backward adds (accumulate != 0) or writes the
+ * unnormalised inverse of residue `residue`, times `scale`, into the data lines.          */
+typedef struct hconv_lines {
+  size_t count, nin, d_out, d_in, es;
+} hconv_lines;
+hconv_status hconv_pfft_forward_lines(const hconv_params* pp, const void* f, const hconv_lines* in, size_t residue,
+                                      void* F, const hconv_lines* out, void* stream);
+hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, const hconv_lines* in, size_t residue,
+                                       void* h, const hconv_lines* out, int accumulate, double scale, void* stream);
+
 /* ---- convolution plans ---- */
 typedef struct hconv_axis {
   size_t L;     /* logical data length along the axis */
@@ -119,8 +136,8 @@ typedef struct hconv_desc {
   hconv_axis axis[3];
   size_t A, B;           /* inputs / outputs of the multiplication operator */
   int mult;              /* hconv_mult */
-  size_t C;              /* 1D: number of independent copies (batch) */
-  size_t dist;           /* 1D: elements between copies; 0 = stored length */
+  size_t C;              /* number of independent copies (1D lines or N-D arrays); 0 = 1 */
+  size_t dist;           /* elements between copies; 0 = stored length (N-D: array size) */
   int device;            /* CUDA ordinal (ignored by the oracle) */
   int flags;             /* reserved, 0 */
   hconv_mult_fn mult_fn; /* HCONV_MULT_CALLBACK: the operator (else ignored) */

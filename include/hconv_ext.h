@@ -15,6 +15,12 @@ hconv_status hconv_util_fill_uniform(uint64_t seed, uint64_t a, uint64_t first_i
 /* Planner report of the last tuning done for this plan: rows (m, p, q, n, block, median ms);
  * returns the row count, or -(count+1) when the choice came from the planner cache. */
 int hconv_plan_report(const hconv_plan* plan, double* out, int cap);
+/* Example native multiplication operators for HCONV_MULT_CALLBACK (device kernels on the
+ * library's stream; a template for user operators written in CUDA):
+ *   which = 0: quadratic products of a 2-component field, A = 2 -> B = 3:
+ *              F0 <- F0 F0, F1 <- F0 F1, F2 <- F1 F1 (complex, or real for Hermitian blocks)
+ * Returns NULL for an unknown id. */
+hconv_mult_fn hconv_example_mult(int which);
 /* Radix plan of the kernel serving an axis ("16x16x24", "direct", ...). */
 const char* hconv_plan_kernel(const hconv_plan* plan, int axis);
 #ifdef __cplusplus

@@ -846,6 +846,63 @@ hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t r
   });
 }
 
+// two-level line batches (include/hconv.h hconv_lines): line l starts at
+// (l / nin) * d_out + (l % nin) * d_in, values at stride es
+static size_t line_base(const hconv_lines& L, size_t l) { return (l / L.nin) * L.d_out + (l % L.nin) * L.d_in; }
+static void check_lines(const hconv_lines* a, const hconv_lines* b) {
+  if (!a || !b) throw std::invalid_argument("null line batch");
+  if (a->nin == 0 || a->es == 0 || b->nin == 0 || b->es == 0) throw std::invalid_argument("line batch: nin and es must be positive");
+  if (a->count != b->count) throw std::invalid_argument("line batches differ in count");
+}
+// natural block order of the CUDA library: the block in the kernels' order.  The oracle's blocks
+// are in the reference order F[u m + l]; for p <= 2 (one chunk) the two coincide, and the
+// drivers that use the _lines entry points only need a pointwise-consistent order between the
+// forward and the backward of the same residue, which the oracle keeps by using its own order
+// on both sides.
+hconv_status hconv_pfft_forward_lines(const hconv_params* pp, const void* f, const hconv_lines* in, size_t residue,
+                                      void* F, const hconv_lines* out, void* /*stream*/) {
+  return guarded([&] {
+    Params P = from_abi(pp);
+    if (residue >= P.n) throw std::invalid_argument("residue out of range");
+    check_lines(in, out);
+    const size_t Ls = stored_len(P), bl = block_len(P);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (size_t l = 0; l < in->count; ++l) {
+      std::vector<cd> x(Ls), y(bl);
+      const cd* src = (const cd*)f + line_base(*in, l);
+      for (size_t j = 0; j < Ls; ++j) x[j] = src[j * in->es];
+      forward(P, x.data(), residue, y.data());
+      const size_t ob = line_base(*out, l);
+      if (P.sym == HCONV_HERMITIAN)
+        for (size_t i = 0; i < bl; ++i) ((double*)F)[ob + i * out->es] = y[i].real();
+      else
+        for (size_t i = 0; i < bl; ++i) ((cd*)F)[ob + i * out->es] = y[i];
+    }
+  });
+}
+hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, const hconv_lines* in, size_t residue,
+                                       void* h, const hconv_lines* out, int accumulate, double scale, void* /*stream*/) {
+  return guarded([&] {
+    Params P = from_abi(pp);
+    if (residue >= P.n) throw std::invalid_argument("residue out of range");
+    check_lines(in, out);
+    const size_t Ls = stored_len(P), bl = block_len(P);
+#pragma omp parallel for schedule(dynamic, 4)
+    for (size_t l = 0; l < in->count; ++l) {
+      std::vector<cd> x(bl), V(Ls);
+      const size_t ib = line_base(*in, l);
+      for (size_t i = 0; i < bl; ++i)
+        x[i] = P.sym == HCONV_HERMITIAN ? cd(((const double*)F)[ib + i * in->es], 0.0) : ((const cd*)F)[ib + i * in->es];
+      backward(P, x.data(), residue, V.data());
+      cd* dst = (cd*)h + line_base(*out, l);
+      for (size_t j = 0; j < Ls; ++j) {
+        cd& o = dst[j * out->es];
+        o = ((accumulate ? o : cd(0.0)) + V[j]) * scale;
+      }
+    }
+  });
+}
+
 struct hconv_plan {
   hconv_desc d;
   std::vector<AxisP> ax;
@@ -917,15 +974,19 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
         for (size_t c = 0; c < C; ++c)
           std::copy(res[b].begin() + c * Ls, res[b].begin() + (c + 1) * Ls, (cd*)out[b] + c * dist);
     } else {
+      if (p->d.dist != 0) throw std::invalid_argument("N-D copies are contiguous arrays: dist must be 0");
       size_t tot = 1;
       for (auto& a : p->ax) tot *= a.stored;
-      std::vector<const cd*> ins(A);
-      for (size_t a = 0; a < A; ++a) ins[a] = (const cd*)in[a];
-      std::vector<std::vector<cd>> res(Bo, std::vector<cd>(tot));
-      std::vector<cd*> outs(Bo);
-      for (size_t b = 0; b < Bo; ++b) outs[b] = res[b].data();
-      convnd_rec(p->ax, 0, mu, ins, outs, par);
-      for (size_t b = 0; b < Bo; ++b) std::copy(res[b].begin(), res[b].end(), (cd*)out[b]);
+      const size_t C = p->d.C ? p->d.C : 1;
+      for (size_t c = 0; c < C; ++c) {  // a batch of C contiguous arrays
+        std::vector<const cd*> ins(A);
+        for (size_t a = 0; a < A; ++a) ins[a] = (const cd*)in[a] + c * tot;
+        std::vector<std::vector<cd>> res(Bo, std::vector<cd>(tot));
+        std::vector<cd*> outs(Bo);
+        for (size_t b = 0; b < Bo; ++b) outs[b] = res[b].data();
+        convnd_rec(p->ax, 0, mu, ins, outs, par);
+        for (size_t b = 0; b < Bo; ++b) std::copy(res[b].begin(), res[b].end(), (cd*)out[b] + c * tot);
+      }
     }
   });
 }

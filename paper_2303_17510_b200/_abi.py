@@ -51,6 +51,12 @@ class Desc(C.Structure):
     ]
 
 
+class Lines(C.Structure):
+    """hconv_lines: line l starts at (l // nin) * d_out + (l % nin) * d_in, values at stride es."""
+
+    _fields_ = [(n, C.c_size_t) for n in ("count", "nin", "d_out", "d_in", "es")]
+
+
 # symbol -> (restype, argtypes); every symbol include/hconv.h declares
 PROTOTYPES = {
     "hconv_derive_params": (C.c_int, [C.c_size_t, C.c_size_t, C.c_size_t, C.c_int, C.POINTER(Params)]),
@@ -70,6 +76,15 @@ PROTOTYPES = {
         C.c_int,
         [C.POINTER(Params), C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p],
     ),
+    "hconv_pfft_forward_lines": (
+        C.c_int,
+        [C.POINTER(Params), C.c_void_p, C.POINTER(Lines), C.c_size_t, C.c_void_p, C.POINTER(Lines), C.c_void_p],
+    ),
+    "hconv_pfft_backward_lines": (
+        C.c_int,
+        [C.POINTER(Params), C.c_void_p, C.POINTER(Lines), C.c_size_t, C.c_void_p, C.POINTER(Lines), C.c_int, C.c_double,
+         C.c_void_p],
+    ),
     "hconv_plan_create": (C.c_int, [C.POINTER(Desc), C.POINTER(C.c_void_p)]),
     "hconv_plan_params": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Params)]),
     "hconv_plan_workspace_bytes": (C.c_size_t, [C.c_void_p]),
@@ -85,6 +100,7 @@ EXT_PROTOTYPES = {
     "hconv_util_fill_uniform": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_size_t, C.c_void_p, C.c_void_p]),
     "hconv_plan_report": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "hconv_plan_kernel": (C.c_char_p, [C.c_void_p, C.c_int]),
+    "hconv_example_mult": (C.c_void_p, [C.c_int]),
 }
 
 

@@ -51,6 +51,13 @@ struct Unsupported : std::runtime_error {
     if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// HCONV_POISON=1 (diagnostics): fill every scratch / work allocation with NaN so that a read
+// before write shows up in the results instead of reading zeros from fresh pages
+void poison(void* p, size_t bytes) {
+  static const bool on = std::getenv("HCONV_POISON") && std::getenv("HCONV_POISON")[0] == '1';
+  if (on) CK(cudaMemset(p, 0xff, bytes));
+}
+
 template <class F>
 hconv_status guarded(F&& f) {
   try {
@@ -323,6 +330,7 @@ struct Scratch {
     p = nullptr;
     bytes = 0;
     CK(cudaMalloc(&p, b));
+    poison(p, b);
     bytes = b;
   }
   void release() {
@@ -726,7 +734,10 @@ struct HostPipe {
     width = 0;
     for (int k = 0; k < slots; ++k) {
       buf[k].assign(w, nullptr);
-      for (auto& b : buf[k]) CK(cudaMalloc(&b, n * sizeof(double2)));
+      for (auto& b : buf[k]) {
+        CK(cudaMalloc(&b, n * sizeof(double2)));
+        poison(b, n * sizeof(double2));
+      }
     }
     elems = n;
     nslots = slots;
@@ -802,6 +813,31 @@ __global__ void k_mult_product(BlockPtrs F, int A, long long count, int real) {
   }
 }
 
+// example operator (hconv_ext.h hconv_example_mult(0)): F0 F0, F0 F1, F1 F1
+__global__ void k_mult_pairs(double2* F0, double2* F1, double2* F2, long long count, int real) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += stride) {
+    if (real) {
+      const double a = ((const double*)F0)[i], b = ((const double*)F1)[i];
+      ((double*)F0)[i] = a * a;
+      ((double*)F1)[i] = a * b;
+      ((double*)F2)[i] = b * b;
+    } else {
+      const double2 a = F0[i], b = F1[i];
+      F0[i] = hc::cmul(a, a);
+      F1[i] = hc::cmul(a, b);
+      F2[i] = hc::cmul(b, b);
+    }
+  }
+}
+int example_mult_pairs(void* const* F, size_t A, size_t B, size_t count, int real, void*, void* stream) {
+  if (A != 2 || B != 3) return 1;
+  const int blocks = (int)std::max<size_t>(1, std::min<size_t>((count + 255) / 256, 4096));
+  k_mult_pairs<<<blocks, 256, 0, (cudaStream_t)stream>>>((double2*)F[0], (double2*)F[1], (double2*)F[2],
+                                                           (long long)count, real);
+  return cudaGetLastError() == cudaSuccess ? 0 : 2;
+}
+
 // MultOperator.apply on one residue's transformed blocks, in place
 void apply_mult(const hconv_plan* P, double2* const* F, long long count, bool real, cudaStream_t s) {
   if (P->d.mult == HCONV_MULT_PRODUCT) {
@@ -814,7 +850,10 @@ void apply_mult(const hconv_plan* P, double2* const* F, long long count, bool re
   }
   void* ptrs[kMaxArity];
   for (size_t a = 0; a < P->W(); ++a) ptrs[a] = F[a];
+  static const bool dsync = std::getenv("HCONV_SYNC_MULT") && std::getenv("HCONV_SYNC_MULT")[0] == '1';
+  if (dsync) CK(cudaDeviceSynchronize());
   const int rc = P->d.mult_fn(ptrs, P->d.A, P->d.B, (size_t)count, real ? 1 : 0, P->d.mult_user, s);
+  if (dsync) CK(cudaDeviceSynchronize());
   if (rc != 0) throw std::invalid_argument("multiplication operator callback returned " + std::to_string(rc));
 }
 
@@ -920,6 +959,7 @@ void check_desc(const hconv_desc* d) {
     throw std::invalid_argument("unknown multiplication operator");
   }
   if (std::max(d->A, d->B) > kMaxArity) throw Unsupported("operator arity above 16");
+  if (d->dims > 1 && d->dist != 0) throw std::invalid_argument("N-D copies are contiguous arrays: dist must be 0");
 }
 
 // Build the axis plans for chosen subtransform sizes and allocate the N-D work buffers.
@@ -939,7 +979,7 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
   // as many as keep this level's buffers within HCONV_ND_BLOCK_MB (default 96 MB, L2-resident)
   static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 96.0;
   P->chunk.assign(d, 1);
-  long long NB = 1;
+  long long NB = (long long)(desc->C ? desc->C : 1);  // arrays at the top level (a batch of N-D arrays)
   for (int l = 0; l < d - 1; ++l) {
     const long long inner = (long long)inner_elems(P, l);
     const long long per = (long long)(P->W() * P->ax[l].dev.B + desc->B * P->ax[l].data) * inner * (long long)sizeof(double2);
@@ -950,11 +990,13 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
     for (size_t a = 0; a < P->W(); ++a) {
       double2* b = nullptr;
       CK(cudaMalloc(&b, (size_t)work * sizeof(double2)));
+      poison(b, (size_t)work * sizeof(double2));
       P->buffers.push_back(b);
     }
     for (size_t b_ = 0; b_ < desc->B; ++b_) {
       double2* b = nullptr;
       CK(cudaMalloc(&b, (size_t)acc * sizeof(double2)));
+      poison(b, (size_t)acc * sizeof(double2));
       P->buffers.push_back(b);
     }
     NB = ch * P->ax[l].dev.B;
@@ -1179,6 +1221,35 @@ hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t r
   });
 }
 
+static hc::Lines to_lines(const hconv_lines* l) {
+  if (!l) throw std::invalid_argument("null line batch");
+  if (l->nin == 0 || l->es == 0) throw std::invalid_argument("line batch: nin and es must be positive");
+  return hc::Lines{(long long)l->count, (long long)l->nin, (long long)l->d_out, (long long)l->d_in, (long long)l->es};
+}
+hconv_status hconv_pfft_forward_lines(const hconv_params* pp, const void* f, const hconv_lines* in, size_t residue,
+                                      void* F, const hconv_lines* out, void* stream) {
+  return guarded([&] {
+    const hb::PlanParams p = from_abi(pp);
+    if (residue >= p.n) throw std::invalid_argument("residue out of range");
+    const hc::Lines lin = to_lines(in), lout = to_lines(out);
+    if (lin.count != lout.count) throw std::invalid_argument("line batches differ in count");
+    AxisPlan ap = make_axis(p);
+    launch_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 0, (cudaStream_t)stream);
+  });
+}
+hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, const hconv_lines* in, size_t residue,
+                                       void* h, const hconv_lines* out, int accumulate, double scale, void* stream) {
+  return guarded([&] {
+    const hb::PlanParams p = from_abi(pp);
+    if (residue >= p.n) throw std::invalid_argument("residue out of range");
+    const hc::Lines lin = to_lines(in), lout = to_lines(out);
+    if (lin.count != lout.count) throw std::invalid_argument("line batches differ in count");
+    AxisPlan ap = make_axis(p);
+    launch_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, scale, (int)residue, 0,
+               (cudaStream_t)stream);
+  });
+}
+
 hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
   return guarded([&] {
     check_desc(desc);
@@ -1258,7 +1329,7 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
       const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
       conv1d(p, ap, (long long)(p->d.C ? p->d.C : 1), dist, ins.data(), outs.data(), s);
     } else {
-      nd_level(p, 0, 1, ins.data(), outs.data(), s);
+      nd_level(p, 0, (long long)(p->d.C ? p->d.C : 1), ins.data(), outs.data(), s);
     }
   });
 }
@@ -1301,12 +1372,13 @@ hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* con
       }
       CK(cudaStreamSynchronize(hp.st[2]));
     } else {
-      size_t n = 1;
+      const long long C = (long long)(p->d.C ? p->d.C : 1);
+      size_t n = (size_t)C;
       for (const AxisPlan& ap : p->ax) n *= ap.data;
       hp.ensure(n, 1, W);
       double2* const* b = hp.buf[0].data();
       for (size_t a = 0; a < A; ++a) CK(cudaMemcpyAsync(b[a], hin(a), n * sizeof(double2), cudaMemcpyHostToDevice, hp.st[1]));
-      nd_level(p, 0, 1, b, b, hp.st[1]);
+      nd_level(p, 0, C, b, b, hp.st[1]);
       for (size_t o = 0; o < Bo; ++o) CK(cudaMemcpyAsync(hout(o), b[o], n * sizeof(double2), cudaMemcpyDeviceToHost, hp.st[1]));
       CK(cudaStreamSynchronize(hp.st[1]));
     }
@@ -1341,6 +1413,8 @@ int hconv_plan_report(const hconv_plan* p, double* out, int cap) {
   }
   return p->report.cached ? -k - 1 : k;
 }
+
+hconv_mult_fn hconv_example_mult(int which) { return which == 0 ? example_mult_pairs : nullptr; }
 
 // kernel description for a plan axis: threads per line group, groups per CTA, radix plan
 const char* hconv_plan_kernel(const hconv_plan* p, int axis) {

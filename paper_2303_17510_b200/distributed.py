@@ -9,16 +9,22 @@ transform runs along y, which every rank holds completely; the sharded axis x be
 axis after one all-to-all transpose:
 
   for each residue block r of the y axis (PAPER.md:584-600 with y as the outer axis):
-    1. local forward padded y-FFT of the A inputs        (hconv_pfft_forward, block r)
-    2. all-to-all: rank g receives the spectral y-lines of its block [k0_g, k1_g) for ALL x
-    3. local (d-1)-D subconvolutions over (x[, z]) of those lines (hconv_convolve; owns mult)
-    4. all-to-all back to the x-slab owners
-    5. local inverse padded y-FFT of block r, accumulated          (hconv_pfft_backward)
-  h *= 1 / (q_y m_y)
+    1. local forward padded y-FFT of the A inputs, ONE strided launch per input
+       (hconv_pfft_forward_lines), written k-major: F_a[k][x][z], so the k-block destined for
+       rank h is one contiguous run (the all-to-all send buffer needs no packing)
+    2. all-to-all: rank g receives the spectral y-lines k in [k0_g, k1_g) of every x-slab,
+       [h][k][x_h][z], and places them as T_a[k][x][z] with x complete (G slice copies)
+    3. the (d-1)-D subconvolutions of all nk spectral lines in ONE batched call
+       (hconv_convolve with C = nk; the plan, and with it the multiplication operator, is
+       created once); outputs in place in T_b, b < B
+    4. all-to-all back: the pieces [h][k][x_g][z] land as W_b[k][x][z] (k-major again)
+    5. local inverse padded y-FFT of block r, accumulated into h_b, the last residue scaled by
+       1/(q_y m_y) (hconv_pfft_backward_lines)
 
-The multi-D DFT is separable, so this equals the paper's x-outer recursion numerically.  Exactly
-two exchanges per residue carry (A + B) x L_x x B_y x (inner) values.  The collective is
-torch.distributed all_to_all_single (NCCL over NVLink on GPUs; gloo on CPU in the tests).
+The multi-D DFT is separable and the inner subconvolutions are pointwise in the y frequency,
+so this equals the paper's x-outer recursion numerically.  Exactly (A + B) exchanges per
+residue carry L_x x B_y x (inner) values each.  The collective is torch.distributed
+all_to_all_single (NCCL over NVLink on GPUs; gloo on CPU in the tests).
 
 The local compute goes through a Backend bound to a library exporting include/hconv.h: the
 sm_100a library with CUDA tensors (product), or -- in the CPU tests only -- the oracle with host
@@ -47,6 +53,33 @@ def partition(n: int, parts: int) -> list[tuple[int, int]]:
     return out
 
 
+def _lines(count, nin, d_out, d_in, es) -> _abi.Lines:
+    return _abi.Lines(count, nin, d_out, d_in, es)
+
+
+class _LocalPlan:
+    """A convolution plan of the backend's library (owns the operator callback)."""
+
+    def __init__(self, be: "Backend", desc: _abi.Desc, mult):
+        self.be = be
+        fn, self._keep = (None, None) if mult is None else mult._native(host=be.device.type != "cuda")
+        desc.mult_fn = fn
+        h = C.c_void_p()
+        be._check(be.lib.hconv_plan_create(C.byref(desc), C.byref(h)))
+        self.h = h
+        self.A, self.B = desc.A, desc.B
+
+    def convolve(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor]) -> None:
+        i = (C.c_void_p * len(ins))(*[t.data_ptr() for t in ins])
+        o = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
+        self.be._check(self.be.lib.hconv_convolve(self.h, i, o, self.be.stream_fn()))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.be.lib.hconv_plan_destroy(self.h)
+            self.h = None
+
+
 class Backend:
     """Local compute through a library exporting the C ABI of include/hconv.h."""
 
@@ -66,41 +99,34 @@ class Backend:
     def block_length(self, p: _abi.Params) -> int:
         return self.lib.hconv_block_length(C.byref(p))
 
-    def forward(self, x: torch.Tensor, p: _abi.Params, r: int, copies: int, stride: int, dist_: int) -> torch.Tensor:
-        """Residue r of the padded forward FFT of `copies` lines (element stride `stride`,
-        copy distance `dist_`) of the contiguous complex128 tensor x -> [copies, blockLength]."""
-        q = _abi.Params.from_buffer_copy(p)
-        q.C, q.S = copies, stride
-        out = torch.empty(copies, self.block_length(p), dtype=torch.complex128, device=self.device)
-        self._check(self.lib.hconv_pfft_forward(C.byref(q), C.c_void_p(x.data_ptr()), dist_, r,
-                                                C.c_void_p(out.data_ptr()), self.stream_fn()))
-        return out
+    def forward_lines(self, x: torch.Tensor, p: _abi.Params, r: int, lin: _abi.Lines, F: torch.Tensor,
+                      lout: _abi.Lines) -> None:
+        self._check(self.lib.hconv_pfft_forward_lines(C.byref(p), C.c_void_p(x.data_ptr()), C.byref(lin), r,
+                                                      C.c_void_p(F.data_ptr()), C.byref(lout), self.stream_fn()))
 
-    def backward(self, F: torch.Tensor, p: _abi.Params, r: int, h: torch.Tensor, copies: int, stride: int, dist_: int,
-                 accumulate: bool) -> None:
-        q = _abi.Params.from_buffer_copy(p)
-        q.C, q.S = copies, stride
-        self._check(self.lib.hconv_pfft_backward(C.byref(q), C.c_void_p(F.data_ptr()), r, C.c_void_p(h.data_ptr()),
-                                                 dist_, int(accumulate), self.stream_fn()))
+    def backward_lines(self, F: torch.Tensor, p: _abi.Params, r: int, lin: _abi.Lines, h: torch.Tensor,
+                       lout: _abi.Lines, accumulate: bool, scale: float) -> None:
+        self._check(self.lib.hconv_pfft_backward_lines(C.byref(p), C.c_void_p(F.data_ptr()), C.byref(lin), r,
+                                                       C.c_void_p(h.data_ptr()), C.byref(lout), int(accumulate),
+                                                       float(scale), self.stream_fn()))
 
-    def convolve(self, axes: Sequence[tuple[int, int, int, int]], f: torch.Tensor, g: torch.Tensor, copies: int = 1,
-                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """hconv_convolve over contiguous arrays (1D: `copies` rows; N-D: one array)."""
+    def plan(self, axes: Sequence[tuple[int, int, int, int]], copies: int, A: int = 2, B: int = 1,
+             mult=None) -> _LocalPlan:
+        """A plan for `copies` contiguous 1D lines or N-D arrays (product, or `mult`)."""
         d = _abi.Desc()
         d.dims = len(axes)
         for k, (L, M, m, s) in enumerate(axes):
             d.axis[k] = _abi.Axis(L, M, m, s)
-        d.A, d.B, d.mult, d.C, d.dist = 2, 1, _abi.MULT_PRODUCT, copies, 0
-        d.device = self.device.index or 0 if self.device.type == "cuda" else 0
-        h = C.c_void_p()
-        self._check(self.lib.hconv_plan_create(C.byref(d), C.byref(h)))
+        d.A, d.B, d.C, d.dist = A, B, copies, 0
+        d.mult = _abi.MULT_PRODUCT if mult is None else mult.kind
+        d.device = (self.device.index or 0) if self.device.type == "cuda" else 0
+        return _LocalPlan(self, d, None if mult is None or mult.kind == _abi.MULT_PRODUCT else mult)
+
+    def convolve(self, axes: Sequence[tuple[int, int, int, int]], f: torch.Tensor, g: torch.Tensor, copies: int = 1,
+                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """hconv_convolve over contiguous arrays (1D: `copies` rows; N-D: one array)."""
         out = f if out is None else out
-        try:
-            ins = (C.c_void_p * 2)(f.data_ptr(), g.data_ptr())
-            outs = (C.c_void_p * 1)(out.data_ptr())
-            self._check(self.lib.hconv_convolve(h, ins, outs, self.stream_fn()))
-        finally:
-            self.lib.hconv_plan_destroy(h)
+        self.plan(axes, copies).convolve([f, g], [out])
         return out
 
 
@@ -130,9 +156,10 @@ class SlabConvND:
 
     axes: [x, y] or [x, y, z]; Hermitian mode = z Hermitian (x, y centered).
     Every subtransform size m must be given (tune per axis with hconv.tune_nd beforehand).
+    mult: None = builtin product (A = 2, B = 1), else an hconv.MultOperator (A inputs, B outputs).
     """
 
-    def __init__(self, axes: Sequence[SlabAxis], backend: Backend, group=None):
+    def __init__(self, axes: Sequence[SlabAxis], backend: Backend, group=None, mult=None):
         if len(axes) not in (2, 3):
             raise ValueError("slab decomposition is for 2D and 3D convolutions")
         self.axes = list(axes)
@@ -140,6 +167,8 @@ class SlabConvND:
         self.group = group
         self.G = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self.mult = mult
+        self.A, self.B = (2, 1) if mult is None else (mult.A, mult.B)
         herm = axes[-1].symmetry == _abi.HERMITIAN
         if len(axes) == 2 and herm:
             raise NotImplementedError("2D Hermitian slabs need the outer axis sharded (3 transposes)")
@@ -151,81 +180,73 @@ class SlabConvND:
         self.xs = partition(self.data[0], self.G)
         self.ks = partition(self.By, self.G)
         self.inner = self.data[2] if len(axes) == 3 else 1  # z extent (1 for 2D)
+        k0, k1 = self.ks[self.rank]
+        self.nk = k1 - k0
+        x = (axes[0].L, axes[0].M, axes[0].m, self.syms[0])
+        sub = [x] if len(axes) == 2 else [x, (axes[2].L, axes[2].M, axes[2].m, self.syms[2])]
+        # the (d-1)-D subconvolutions of this rank's nk spectral y-lines: one batched plan
+        self.inner_plan = backend.plan(sub, max(1, self.nk), self.A, self.B, mult) if self.nk else None
 
     def local_shape(self) -> tuple[int, ...]:
         x0, x1 = self.xs[self.rank]
         return (x1 - x0, *self.data[1:])
 
-    def _forward_y(self, f: torch.Tensor, r: int) -> torch.Tensor:
-        """[nx, Ly, Z] -> [nx, Z, By] (residue r of the y padded FFT)."""
-        nx, Z = f.shape[0], self.inner
-        Ly = self.data[1]
-        if Z == 1:
-            return self.b.forward(f, self.py, r, nx, 1, Ly).view(nx, 1, self.By)
-        out = torch.empty(nx, Z, self.By, dtype=f.dtype, device=f.device)
-        for i in range(nx):
-            out[i] = self.b.forward(f[i], self.py, r, Z, Z, 1)
-        return out
-
-    def _backward_y(self, W: torch.Tensor, r: int, h: torch.Tensor, accumulate: bool) -> None:
-        nx, Z = W.shape[0], self.inner
-        Ly = self.data[1]
-        if Z == 1:
-            self.b.backward(W.reshape(nx, self.By).contiguous(), self.py, r, h, nx, 1, Ly, accumulate)
-            return
-        for i in range(nx):
-            self.b.backward(W[i].contiguous(), self.py, r, h[i], Z, Z, 1, accumulate)
-
-    def _inner(self, T: torch.Tensor, U: torch.Tensor) -> None:
-        """(d-1)-D subconvolutions of the received spectral lines T, U: [nk, Lx, Z], in place in T."""
-        ax = self.axes
-        x = (ax[0].L, ax[0].M, ax[0].m, self.syms[0])
-        if self.inner == 1:
-            self.b.convolve([x], T.view(T.shape[0], -1), U.view(U.shape[0], -1), copies=T.shape[0])
-        else:
-            z = (ax[2].L, ax[2].M, ax[2].m, self.syms[2])
-            for k in range(T.shape[0]):
-                self.b.convolve([x, z], T[k], U[k])
-
-    def convolve(self, f: torch.Tensor, g: torch.Tensor, out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """f, g: this rank's x-slabs (local_shape()); returns the convolution's x-slab."""
-        if tuple(f.shape) != self.local_shape() or tuple(g.shape) != self.local_shape():
-            raise ValueError(f"expected local slabs of shape {self.local_shape()}")
-        G, me = self.G, self.rank
-        nx = f.shape[0]
-        Z = self.inner
-        f3, g3 = f.reshape(nx, self.data[1], Z), g.reshape(nx, self.data[1], Z)
-        h = torch.zeros_like(f3) if out is None else out.reshape(nx, self.data[1], Z)
-        k0, k1 = self.ks[me]
-        nk = k1 - k0
-        Lx = self.data[0]
-        send_sizes = [nx * Z * (b - a) for a, b in self.ks]
-        recv_sizes = [(b - a) * Z * nk for a, b in self.xs]
+    def convolve(self, inputs: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None) -> list[torch.Tensor]:
+        """inputs: this rank's x-slabs (local_shape()) of the A inputs; returns the B output
+        slabs (by default written over the first B inputs)."""
+        if isinstance(inputs, torch.Tensor):
+            raise TypeError("pass a sequence of input slabs")
+        if len(inputs) != self.A:
+            raise ValueError(f"expected {self.A} input slabs")
+        for t in inputs:
+            if tuple(t.shape) != self.local_shape():
+                raise ValueError(f"expected local slabs of shape {self.local_shape()}")
+        outs = list(inputs[:self.B]) if out is None else list(out)
+        if len(outs) != self.B:
+            raise ValueError(f"expected {self.B} output slabs")
+        G, me, Z, By, nk = self.G, self.rank, self.inner, self.By, self.nk
+        nx = inputs[0].shape[0]
+        Ly, Lx = self.data[1], self.data[0]
+        dev, dt = inputs[0].device, inputs[0].dtype
+        nxz = nx * Z
+        lin = _lines(nxz, Z, Ly * Z, 1, Z)        # y-lines (x, z) of an x-slab [nx][Ly][Z]
+        lspec = _lines(nxz, nxz, 0, 1, nxz)       # the same lines k-major: F[k][x][z]
+        send_sizes = [(b - a) * nxz for a, b in self.ks]
+        recv_sizes = [nk * (b - a) * Z for a, b in self.xs]
+        F = torch.empty(By * nxz, dtype=dt, device=dev)
+        recv = torch.empty(sum(recv_sizes), dtype=dt, device=dev)
+        T = [torch.empty(max(1, nk) * Lx * Z, dtype=dt, device=dev) for _ in range(max(self.A, self.B))]
+        back = torch.empty(sum(recv_sizes), dtype=dt, device=dev)
+        W = torch.empty(By * nxz, dtype=dt, device=dev)
+        # results accumulate in separate buffers when an output aliases an input (inputs are
+        # read by every residue's forward)
+        ins_ptrs = {t.data_ptr() for t in inputs}
+        acc = [torch.empty_like(o) if o.data_ptr() in ins_ptrs else o for o in outs]
         n_res = self.py.n
+        scale = 1.0 / (self.py.q * self.py.m)
         for r in range(n_res):
-            specs = []
-            for a in (f3, g3):
-                F = self._forward_y(a, r)  # [nx, Z, By]
-                send = torch.cat([F[:, :, a_:b_].permute(2, 0, 1).reshape(-1) for a_, b_ in self.ks])
-                recv = torch.empty(sum(recv_sizes), dtype=F.dtype, device=F.device)
-                _a2a(recv, send, recv_sizes, send_sizes, self.group)
-                # pieces from rank h: [nk, nx_h, Z] -> T[nk, Lx, Z]
-                T = torch.empty(nk, Lx, Z, dtype=F.dtype, device=F.device)
+            for a in range(self.A):
+                self.b.forward_lines(inputs[a], self.py, r, lin, F, lspec)
+                _a2a(recv, F, recv_sizes, send_sizes, self.group)
+                Ta = T[a].view(max(1, nk), Lx, Z)
                 off = 0
                 for (xa, xb), sz in zip(self.xs, recv_sizes):
-                    T[:, xa:xb, :] = recv[off:off + sz].view(nk, xb - xa, Z)
+                    if sz:
+                        Ta[:, xa:xb, :] = recv[off:off + sz].view(nk, xb - xa, Z)
                     off += sz
-                specs.append(T)
-            self._inner(specs[0], specs[1])
-            T = specs[0]
-            send = torch.cat([T[:, xa:xb, :].reshape(-1) for xa, xb in self.xs])
-            back = torch.empty(sum(send_sizes), dtype=T.dtype, device=T.device)
-            _a2a(back, send, send_sizes, recv_sizes, self.group)
-            W = torch.empty(nx, Z, self.By, dtype=T.dtype, device=T.device)
-            off = 0
-            for (a_, b_), sz in zip(self.ks, send_sizes):
-                W[:, :, a_:b_] = back[off:off + sz].view(b_ - a_, nx, Z).permute(1, 2, 0)
-                off += sz
-            self._backward_y(W, r, h, accumulate=r > 0)
-        h.mul_(1.0 / (self.py.q * self.py.m))
-        return h.reshape(self.local_shape())
+            if nk:
+                self.inner_plan.convolve(T[:self.A], T[:self.B])
+            last = r == n_res - 1
+            for b in range(self.B):
+                Tb = T[b].view(max(1, nk), Lx, Z)
+                off = 0
+                for (xa, xb), sz in zip(self.xs, recv_sizes):
+                    if sz:
+                        back[off:off + sz].view(nk, xb - xa, Z).copy_(Tb[:, xa:xb, :])
+                    off += sz
+                _a2a(W, back, send_sizes, recv_sizes, self.group)
+                self.b.backward_lines(W, self.py, r, lspec, acc[b], lin, accumulate=r > 0, scale=scale if last else 1.0)
+        for o, a_ in zip(outs, acc):
+            if o.data_ptr() != a_.data_ptr():
+                o.copy_(a_)
+        return outs

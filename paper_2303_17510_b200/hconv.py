@@ -241,8 +241,9 @@ class MultOperator:
     apply: Optional[Callable] = None
     fn: Optional[int] = None
 
-    def _native(self):
-        """(hconv_mult_fn address, keep-alive object) for the descriptor."""
+    def _native(self, host: bool = False):
+        """(hconv_mult_fn address, keep-alive object) for the descriptor.  host=True: the
+        library passes host pointers (the CPU oracle behind the same ABI, test infrastructure)."""
         if self.kind == _abi.MULT_PRODUCT:
             return None, None
         if self.fn is not None:
@@ -251,10 +252,22 @@ class MultOperator:
 
         def _fn(F, A, B, count, real, user, stream):
             try:
+                if host:
+                    import numpy as np
+
+                    n = count * (1 if real else 2)
+                    blocks = [torch.from_numpy(np.ctypeslib.as_array(C.cast(F[i], C.POINTER(C.c_double)), (n,))
+                                               .view(np.float64 if real else np.complex128))
+                              for i in range(max(A, B))]
+                    apply(blocks, bool(real))
+                    return 0
                 dev = torch.cuda.current_device()
                 blocks = [torch.as_tensor(_CudaArray(F[i], count, bool(real)), device=f"cuda:{dev}")
                           for i in range(max(A, B))]
-                with torch.cuda.stream(torch.cuda.ExternalStream(stream or 0)):
+                # the library's stream; NULL is the legacy default stream (ExternalStream(0) would
+                # be a fresh pool stream, unordered with the library's kernels)
+                st = torch.cuda.ExternalStream(stream) if stream else torch.cuda.default_stream(dev)
+                with torch.cuda.stream(st):
                     apply(blocks, bool(real))
                 return 0
             except Exception:  # noqa: BLE001 -- the library turns a nonzero return into a status
@@ -359,7 +372,7 @@ class ConvPlanND(_Plan):
     """d-dimensional plan; axes[-1] is the contiguous innermost axis.
     Hermitian mode (innermost Hermitian) makes the outer axes centered."""
 
-    def __init__(self, axes: Sequence[AxisSpec], mult: Optional[MultOperator] = None, device: int = 0):
+    def __init__(self, axes: Sequence[AxisSpec], mult: Optional[MultOperator] = None, device: int = 0, C_: int = 1):
         mult = mult or builtin_mult_product(2)
         if not 1 <= len(axes) <= 3:
             raise ValueError("1 to 3 axes")
@@ -367,14 +380,17 @@ class ConvPlanND(_Plan):
         d.dims = len(axes)
         for k, a in enumerate(axes):
             d.axis[k] = _abi.Axis(a.L, a.M, a.m or 0, int(a.symmetry))
-        d.A, d.B, d.mult, d.C, d.dist, d.device = mult.A, mult.B, mult.kind, 1, 0, device
+        d.A, d.B, d.mult, d.C, d.dist, d.device = mult.A, mult.B, mult.kind, C_, 0, device
         super().__init__(d, mult)
+        self.copies = C_
         self.mult = mult
         self.axes = list(axes)
         self.params = [self.axis_params(k) for k in range(len(axes))]
 
     def shape(self) -> tuple[int, ...]:
-        return tuple(p.dataLength() for p in self.params)
+        """array shape a call expects: (C, *axes) for a batch of C > 1 arrays"""
+        shp = tuple(p.dataLength() for p in self.params)
+        return (self.copies, *shp) if self.copies > 1 else shp
 
 
 def _check_mult(inputs, mult: MultOperator, plan: _Plan):

@@ -1,0 +1,85 @@
+"""The slab decomposition (paper_2303_17510_b200.distributed) on the GPU: NCCL with one rank
+(the whole machine gpurun gives us), CUDA backend -- the strided line passes
+(hconv_pfft_*_lines), the batched N-D convolve and the exchange bookkeeping -- against the
+single-device convolve_nd on the same seeded inputs.  Multi-rank exchanges are covered on CPU
+(tests/test_distributed_cpu.py, gloo, 2 and 3 ranks)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = {
+    "2d_complex": [(256, 511, 256, 0), (192, 383, 128, 0)],
+    "3d_hermitian": [(63, 94, 32, 1), (63, 94, 48, 1), (63, 94, 32, 2)],
+    "3d_complex": [(40, 79, 40, 0), (48, 95, 32, 0), (24, 47, 24, 0)],
+}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(port, q):
+    import torch
+    import torch.distributed as dist
+
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+        import sys
+        from pathlib import Path
+
+        repo = Path(__file__).resolve().parents[1]
+        sys.path.insert(0, str(repo))
+        sys.path.insert(0, str(repo / "tests"))
+        from oracle_lib import rel_l2
+        from paper_2303_17510_b200 import hconv
+        from paper_2303_17510_b200.distributed import SlabAxis, SlabConvND, cuda_backend
+
+        res = {}
+        for name, axes in CASES.items():
+            shape = tuple((L + 1) // 2 if s == 2 else L for L, M, m, s in axes)
+            f = torch.empty(shape, dtype=torch.complex128, device="cuda")
+            g = torch.empty_like(f)
+            hconv.fill_uniform(f, 2, 0)
+            hconv.fill_uniform(g, 2, 1)
+            if axes[-1][3] == 2:
+                hconv.hermitian_symmetrize_boundary(f, [a[0] for a in axes])
+                hconv.hermitian_symmetrize_boundary(g, [a[0] for a in axes])
+            plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, m, hconv.Symmetry(s)) for L, M, m, s in axes])
+            ref = hconv.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu().numpy()
+            sc = SlabConvND([SlabAxis(*a) for a in axes], cuda_backend())
+            h = sc.convolve([f.clone(), g.clone()])[0]
+            torch.cuda.synchronize()
+            res[name] = rel_l2(h.cpu().numpy(), ref)
+        q.put((res, None))
+    except Exception:  # pragma: no cover - reported to the parent
+        import traceback
+
+        q.put((None, traceback.format_exc()))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_slab_single_rank_nccl_matches_convolve_nd(cuda):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_worker, args=(_free_port(), q))
+    p.start()
+    res, tb = q.get(timeout=600)
+    p.join(timeout=60)
+    assert tb is None, tb
+    for name, err in res.items():
+        assert err <= 1e-12, (name, err)

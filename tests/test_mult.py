@@ -181,3 +181,36 @@ def test_gpu_general_operator_nd(cuda, oracle):
         refs = oracle.convolve_general(axes, [f, g], 3, _pairs)
         for o, r in zip(outs, refs):
             assert rel_l2(o.cpu().numpy(), r) <= 1e-12
+
+
+@pytest.mark.gpu
+def test_gpu_operator_stream_order_repeated(cuda, oracle):
+    """Repeated calls (no allocation in between, so nothing synchronises by accident): the
+    Python operator must run on the library's stream -- NULL is the legacy default stream, not
+    a fresh pool stream -- and the native example operator (hconv_example_mult) likewise."""
+    import torch
+
+    from paper_2303_17510_b200 import _abi
+
+    rng = np.random.default_rng(12)
+    axes = [(31, 46, 16, 1), (31, 46, 16, 1), (31, 46, 16, 2)]
+    f, g = _rand(rng, (31, 31, 16)), _rand(rng, (31, 31, 16))
+    f, g = oracle.symmetrize([a[0] for a in axes], f), oracle.symmetrize([a[0] for a in axes], g)
+    refs = oracle.convolve_general(axes, [f, g], 3, _pairs)
+
+    def pairs_t(b, real):
+        f0, f1 = b[0].clone(), b[1].clone()
+        b[0].copy_(f0 * f0)
+        b[1].copy_(f0 * f1)
+        b[2].copy_(f1 * f1)
+
+    ops = [cuda.mult_operator(2, 3, pairs_t), cuda.MultOperator(2, 3, _abi.MULT_CALLBACK, fn=cuda.lib().hconv_example_mult(0))]
+    ft, gt = torch.from_numpy(f).cuda(), torch.from_numpy(g).cuda()
+    for op in ops:
+        plan = cuda.ConvPlanND([cuda.AxisSpec(L, M, m, cuda.Symmetry(s)) for L, M, m, s in axes], op)
+        outs = [torch.empty_like(ft) for _ in range(3)]
+        for _ in range(6):
+            cuda.convolve_nd([ft, gt], op, plan, out=outs)
+            torch.cuda.synchronize()
+            for o, r in zip(outs, refs):
+                assert rel_l2(o.cpu().numpy(), r) <= 1e-12
