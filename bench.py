@@ -226,10 +226,13 @@ def run_cuda(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.slab:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29577")
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     name = args.config
     dims, axes, C_, shape, n_out = config_sizes(name)
     stream = torch.cuda.current_stream()
@@ -239,28 +242,51 @@ def run_cuda(args):
     if args.m:
         vals = [int(x) for x in str(args.m).split(",")]
         ms = vals if len(vals) == dims else [vals[0]] * dims
+    # 2D/3D over several GPUs: x-slabs, NCCL all-to-all (strong scaling); --slab forces the slab
+    # path at one rank (exercises the decomposition on a single GPU)
+    slab = dims > 1 and (world > 1 or args.slab)
     if dims == 1:
         L, M, s = axes[0]
         plan = hconv.Conv1dPlan(L, M, ms[0], hconv.Symmetry(s), C_=C_, device=local)
         params = [plan.params]
     else:
-        plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, mk, hconv.Symmetry(s)) for (L, M, s), mk in zip(axes, ms)],
-                                device=local)
+        # the planner runs on rank 0 and every rank uses its choice (the y blocks must agree)
+        chosen = [None]
+        if rank == 0 or not slab:
+            plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, mk, hconv.Symmetry(s)) for (L, M, s), mk in zip(axes, ms)],
+                                    device=local)
+            chosen = [[p.m for p in plan.params]]
+        if slab:
+            import torch.distributed as dist
+
+            dist.broadcast_object_list(chosen, src=0)
+            plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, mk, hconv.Symmetry(s)) for (L, M, s), mk in zip(axes, chosen[0])],
+                                    device=local)
         params = plan.params
     full_shape = (C_, *shape) if dims == 1 else tuple(shape)
     f = torch.empty(full_shape, dtype=torch.complex128, device=dev)
     g = torch.empty_like(f)
-    out = torch.empty_like(f)
-    first = rank * f.numel()  # each rank owns its own slice of the global batch
+    first = rank * f.numel() if not slab else 0  # 1D: each rank owns its own slice of the global batch
     hconv.fill_uniform(f, 1, 0, first)
     hconv.fill_uniform(g, 1, 1, first)
     if dims == 3:
         hconv.hermitian_symmetrize_boundary(f, [L for (L, M, s) in axes])
         hconv.hermitian_symmetrize_boundary(g, [L for (L, M, s) in axes])
+    sc = None
+    if slab:
+        from paper_2303_17510_b200.distributed import SlabAxis, SlabConvND, cuda_backend
+
+        sc = SlabConvND([SlabAxis(L, M, p.m, s) for (L, M, s), p in zip(axes, params)], cuda_backend(dev))
+        x0, x1 = sc.xs[rank]
+        f, g = f[x0:x1].clone(), g[x0:x1].clone()  # this rank's x-slabs of the global arrays
+        torch.cuda.empty_cache()
+    out = torch.empty_like(f)
 
     def step():
         if dims == 1:
             hconv.convolve([f, g], plan.mult, plan, out=out)
+        elif slab:
+            sc.convolve([f, g], out=[out])
         else:
             hconv.convolve_nd([f, g], plan.mult, plan, out=out)
 
@@ -291,7 +317,8 @@ def run_cuda(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * n_out * args.steps / (ms * 1e-3)
+    # 1D: every rank convolves its own batch (weak scaling); slabs: the ranks share one problem
+    value = (1 if slab else world) * n_out * args.steps / (ms * 1e-3)
 
     # e2e through the public host-buffer API (hconv.convolve_host, the reference's calling
     # convention): every step copies both inputs from pinned host memory to the device and the
@@ -301,7 +328,12 @@ def run_cuda(args):
     ho = torch.empty_like(hf).pin_memory()
 
     def step_host():
-        hconv.convolve_host([hf, hg], plan.mult, plan, out=ho)
+        if slab:  # host slabs in, device convolution, host slab out
+            fd, gd = hf.to(dev, non_blocking=True), hg.to(dev, non_blocking=True)
+            ho.copy_(sc.convolve([fd, gd])[0], non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+        else:
+            hconv.convolve_host([hf, hg], plan.mult, plan, out=ho)
 
     for _ in range(2):
         step_host()
@@ -323,7 +355,7 @@ def run_cuda(args):
         t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-    e2e_value = world * n_out * e2e_steps / (e2e_ms * 1e-3)
+    e2e_value = (1 if slab else world) * n_out * e2e_steps / (e2e_ms * 1e-3)
 
     if rank != 0:
         if world > 1:
@@ -333,6 +365,8 @@ def run_cuda(args):
         return
     hbm, src_h, fp64, src_f = peaks()
     nbytes, flops = algorithmic(name)
+    if slab:  # per-GPU share of the one global problem (the roofline is per GPU)
+        nbytes, flops = nbytes / world, flops / world
     t_s = ms_step * 1e-3
     achieved_tf = flops / t_s / 1e12
     t_roof = max(nbytes / (hbm * 1e9), flops / (fp64 * 1e12))
@@ -341,13 +375,17 @@ def run_cuda(args):
     if tp.exists():
         traffic = json.loads(tp.read_text()).get("dram_bytes_per_launch")
     launches = args.steps * launches_per_step(params)
+    if slab:  # per y residue: A forward + the batched subconvolutions + B backward (torch copies not counted)
+        launches = args.steps * params[1].n * (A + launches_per_step([params[0]] + params[2:]) + B)
     line = {
         "metric": "complex128 dealiased-convolution output points/s",
         "value": value, "unit": "points/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "complex128 (f64)", "data": "synthetic (counter-based uniform[-1,1], seed 1; each rank its own batch slice)",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if slab else "weak", "vs_baseline": None,
+        "dtype": "complex128 (f64)",
+        "data": "synthetic (counter-based uniform[-1,1], seed 1; " + ("x-slabs of one global problem)" if slab else "each rank its own batch slice)"),
         "config": {
-            "workload": WORKLOAD[name], "config": name, "batch_per_gpu": C_, "global_batch": C_ * world,
+            "workload": WORKLOAD[name], "config": name, "batch_per_gpu": C_, "global_batch": C_ * (1 if slab else world),
+            "parallelism": (f"x-slabs over {world} GPUs, NCCL all-to-all per y residue" if slab else f"dp{world} (independent batches)"),
             "plan": [dict(m=p.m, p=p.p, q=p.q, n=p.n, block=p.blockLength(), regime=p.regime.name) for p in params],
             "kernel": plan.kernel(len(params) - 1),
             "l2": "inputs+output larger than L2 (3 x 393 MB vs 126 MB)" if name == "c2" else "see config",
@@ -375,7 +413,7 @@ def run_cuda(args):
         except SystemExit as e:
             line["cpu_baseline"] = {"value": None, "unit": "points/s", "cores": os.cpu_count(), "kind": "port", "sample": str(e)}
     print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or args.slab:
         import torch.distributed as dist
 
         dist.destroy_process_group()
@@ -390,6 +428,7 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--m", default=None, help="force subtransform size(s): one value or one per axis, comma separated")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--slab", action="store_true", help="2D/3D: run the x-slab decomposition even on one rank")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
