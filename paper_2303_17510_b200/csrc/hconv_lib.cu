@@ -868,7 +868,8 @@ void conv1d_general(hconv_plan* P, const AxisPlan& ap, long long C, long long di
   const size_t A = P->d.A, Bo = P->d.B, W = P->W();
   const long long Bl = ap.dev.B, S = (long long)ap.data, n = ap.dev.n;
   const bool real = ap.dev.sym == hc::SYM_HERMITIAN;
-  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 96.0;
+  // work blocks per pass: HCONV_GENERAL_BLOCK_MB (default 256 MB of blocks and accumulators)
+  static const double block_mb = std::getenv("HCONV_GENERAL_BLOCK_MB") ? std::atof(std::getenv("HCONV_GENERAL_BLOCK_MB")) : 256.0;
   const long long per_line = (long long)(W * Bl + (n > 1 ? Bo * dist : 0)) * (long long)sizeof(double2);
   const long long chunk = std::max<long long>(1, std::min<long long>(C, (long long)(block_mb * 1048576.0 / per_line)));
   const long long acc_elems = (chunk - 1) * dist + S;
@@ -976,8 +977,10 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
     return;
   }
   // level l processes `chunk[l]` arrays per pass: all of them at the top level, and below it
-  // as many as keep this level's buffers within HCONV_ND_BLOCK_MB (default 96 MB, L2-resident)
-  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 96.0;
+  // as many as keep this level's buffers within HCONV_ND_BLOCK_MB (0 = all of them)
+  // (B200, c5: chunks of 96 MB 13.7 ms, 1 GB 11.8 ms, unchunked 11.6 ms -- the small per-chunk
+  // launches lose more to tails than L2 residency saves -- so blocking is off by default)
+  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 0.0;
   P->chunk.assign(d, 1);
   long long NB = (long long)(desc->C ? desc->C : 1);  // arrays at the top level (a batch of N-D arrays)
   for (int l = 0; l < d - 1; ++l) {

@@ -31,7 +31,12 @@ import torch
 
 from . import _abi
 
-LIB_PATH = _abi.ROOT / "_lib" / "libhconv_cuda.so"
+import os as _os
+
+# HCONV_LIB_VARIANT=name loads _lib_<name>/libhconv_cuda.so (A/B builds of the same sources with
+# different compile-time options, `make VARIANT=name EXTRA=...`); default: the product build
+LIB_PATH = _abi.ROOT / ("_lib_" + _os.environ["HCONV_LIB_VARIANT"] if _os.environ.get("HCONV_LIB_VARIANT") else "_lib") \
+    / "libhconv_cuda.so"
 _lib: Optional[C.CDLL] = None
 _lock = threading.Lock()
 
