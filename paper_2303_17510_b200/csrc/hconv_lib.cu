@@ -390,7 +390,10 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
                  Scratch& scratch, cudaStream_t s) {
   if (lin.count == 0) return;
   const ConvLayout cl = conv_layout(ap, lin);
-  const void* fn = cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
+  // the paired ping-pong kernel where it exists (complex, L <= B; registry) -- HCONV_PP2=0 disables it
+  static const bool pp2_on = !(std::getenv("HCONV_PP2") && std::getenv("HCONV_PP2")[0] == '0');
+  const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
+  const void* fn = pp2 ? ap.k->convpp2_fn : cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
   const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
   hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr, 0};
@@ -409,7 +412,8 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
     CK(cudaMemset(tbuf, 0, 256 * sizeof(unsigned long long)));
     a.trace = tbuf;
   }
-  if (cl.stage == 3) ap.k->convpp(a, grid, cl.smem, s);
+  if (pp2) ap.k->convpp2(a, grid, cl.smem, s);
+  else if (cl.stage == 3) ap.k->convpp(a, grid, cl.smem, s);
   else ap.k->conv(a, grid, cl.smem, s);
   CK(cudaGetLastError());
   if (tbuf) {

@@ -763,6 +763,268 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
 #undef HC_TRACE
 }
 
+// ------------------------------------------------- conv1d, ping-pong, paired --
+// Complex lines with L <= B (no folding) in kernels that own the SM (X, Y and TMEM): the f and g
+// forward FFTs run as ONE interleaved pair (fft_forward_pair: f's exchanges in X, g's in Y, half
+// the barrier phases of two transforms, and one stream's butterflies overlap the other's
+// shared-memory traffic); the product needs no stash.  TMEM keeps the residue accumulator and,
+// for residues after the first, g's raw pass-0 values (the next residue re-reads only f).
+//   copies: next f into X right after the pair's last exchange (a whole inverse of lead time);
+//   next line's g into Y right after the inverse's last exchange, from L2 (prefetched at the
+//   start of the line's last inverse); the last residue writes its outputs straight from
+//   registers (streaming stores), so Y is free as soon as the inverse is done.
+template <class Cfg>
+__device__ __forceinline__ void load_raw_pp2(double2 (&v)[Cfg::E], int L, const double2* X, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
+  sfor<C0>([&](auto Ci) HC_INL {
+    constexpr int c = Ci;
+    const int b = tid + c * Cfg::T;
+    if (bvalid<Cfg, 0>(c, tid))
+      sfor<R0>([&](auto Ai) HC_INL {
+        const int s = Ns1 * Ai + b;
+        v[c * R0 + Ai] = s < L ? X[s] : make_double2(0.0, 0.0);
+      });
+  });
+}
+template <class Cfg, int DIR>
+__device__ __forceinline__ void twiddle_u_pp2(double2 (&v)[Cfg::E], const double2* U, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0);
+  sfor<C0>([&](auto Ci) HC_INL {
+    constexpr int c = Ci;
+    if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { v[c * R0 + Ai] = mul_tw<DIR>(v[c * R0 + Ai], U[Ai]); });
+  });
+}
+
+// fft_forward_pair with the LAST pass split: passes 0 .. P-2 run paired (f through X, g through
+// Y), then f's last-pass DFT runs alone and its spectrum is stashed (stash_f, e.g. to TMEM),
+// then g's: at most one stream's last-pass values are live at a time (radix plans whose last
+// pass holds more values per thread than two streams fit in registers, 16x16x24 at 384
+// threads).  hook() runs once X is free (f's last-pass inputs loaded by every thread); Y is
+// read by the time the function returns (the caller synchronises before reusing it).
+template <class Cfg, class Sync, class P0, class Hook, class StashF>
+__device__ __forceinline__ void fft_forward_pair_split(double2 (&v)[Cfg::E], double2 (&w)[Cfg::E], double2* X, double2* Y,
+                                                       const double2* mt, int tid, const Sync& sync, const P0& p0,
+                                                       const Hook& hook, const StashF& stash_f) {
+  constexpr int P = Cfg::P, T = Cfg::T;
+  static_assert(P >= 2, "radix plans have at least two passes");
+  sfor<P - 1>([&](auto I) HC_INL {
+    constexpr int i = I;
+    constexpr int R = Cfg::R(i), C = Cfg::C(i), NB = Cfg::NB(i), Ns1 = Cfg::Ns(i + 1), Rp = Cfg::Rprod(i);
+    sfor<C>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (NB % T == 0 || beta < NB) {
+        DFT<R, +1>::run(v + c * R);
+        DFT<R, +1>::run(w + c * R);
+        if constexpr (i == 0) {
+          double2 t, tw;
+          p0(beta, t, tw);
+          sfor<R>([&](auto Ki) HC_INL {
+            constexpr int k = Ki;
+            v[c * R + k] = cmul(v[c * R + k], t);
+            w[c * R + k] = cmul(w[c * R + k], t);
+            if constexpr (k + 1 < R) t = cmul(t, tw);
+          });
+        } else {
+          const int b = beta % Ns1;
+          sfor<R - 1>([&](auto Ki) HC_INL {
+            constexpr int k = Ki + 1;
+            const double2 tw = mt[Cfg::MTo(i) + (k - 1) * Ns1 + b];
+            v[c * R + k] = cmul(v[c * R + k], tw);
+            w[c * R + k] = cmul(w[c * R + k], tw);
+          });
+        }
+        const int K = beta / Ns1, b = beta % Ns1;
+        constexpr int St = Cfg::St(i + 1);
+        sfor<R>([&](auto Ki) HC_INL {
+          X[(K + Rp * Ki) * St + b] = v[c * R + Ki];
+          Y[(K + Rp * Ki) * St + b] = w[c * R + Ki];
+        });
+      }
+    });
+    sync();
+    constexpr int R2 = Cfg::R(i + 1), C2 = Cfg::C(i + 1), NB2 = Cfg::NB(i + 1), Ns2 = Cfg::Ns(i + 2);
+    constexpr int St = Cfg::St(i + 1);
+    if constexpr (i + 1 < P - 1) {
+      sfor<C2>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB2 % T == 0 || beta < NB2) {
+          const int K = beta / Ns2, b = beta % Ns2;
+          sfor<R2>([&](auto Ai) HC_INL {
+            v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b];
+            w[c * R2 + Ai] = Y[K * St + Ns2 * Ai + b];
+          });
+        }
+      });
+      sync();
+    } else {
+      // last pass: f alone (X), stash, then g (Y)
+      sfor<C2>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB2 % T == 0 || beta < NB2) {
+          const int K = beta / Ns2, b = beta % Ns2;
+          sfor<R2>([&](auto Ai) HC_INL { v[c * R2 + Ai] = X[K * St + Ns2 * Ai + b]; });
+        }
+      });
+      sync();
+      hook();
+      sfor<C2>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        if (NB2 % T == 0 || tid + c * T < NB2) DFT<R2, +1>::run(v + c * R2);
+      });
+      stash_f(v);
+      sfor<C2>([&](auto Ci) HC_INL {
+        constexpr int c = Ci;
+        const int beta = tid + c * T;
+        if (NB2 % T == 0 || beta < NB2) {
+          const int K = beta / Ns2, b = beta % Ns2;
+          sfor<R2>([&](auto Ai) HC_INL { w[c * R2 + Ai] = Y[K * St + Ns2 * Ai + b]; });
+          DFT<R2, +1>::run(w + c * R2);
+        }
+      });
+    }
+  });
+}
+
+template <class Cfg, int G, int MINB = 1>
+__global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp2(ConvArgs p) {
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2 * G];
+  __shared__ uint32_t tm_base;
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1);
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), E0 = C0 * R0, Ns1 = Cfg::Ns(1);
+  // split last pass (more than 16 last-pass values per thread): f's spectrum parks in TMEM in
+  // place of g's raw values (TMEM holds 512 columns), and g is re-copied for every residue
+  constexpr bool SPLIT = Cfg::ES > 16;
+  using TL = TmemLayout<T * G, SPLIT ? Cfg::ES : E0, E0>;  // g raw (or f spectrum), accumulator
+  static_assert(TL::FITS, "TMEM layout");
+  const int g = threadIdx.x / T, tid = threadIdx.x % T;
+  double2* tb = smem;
+  const double2* mt = tb;
+  double2* X = smem + p.ax.tabn + g * p.gs;
+  double2* Y = X + Cfg::XS;
+  uint64_t* bar_f = &bars[2 * g];
+  uint64_t* bar_g = &bars[2 * g + 1];
+  const GroupSync sync{g + 1, T};
+  const AxisDev& a = p.ax;
+  stage_tables(tb, a, a.tabn);
+  if (tid == 0) {
+    mbar_init(bar_f, 1);
+    mbar_init(bar_g, 1);
+    fence_mbar_init();
+  }
+  // TMEM only with several residues (g stash, accumulator); every CTA resident on the SM fits
+  // its columns (registry: pp2 instantiated only when they do)
+  const bool use_tm = a.n > 1;
+  if (use_tm && threadIdx.x < 32) tmem_alloc(&tm_base, TL::COLS);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tg = use_tm ? TL::f_addr(tm_base) : 0u, ta = use_tm ? TL::a_addr(tm_base) : 0u, tf = tg;
+  uint32_t ph_f = 0, ph_g = 0;
+  const uint32_t row_bytes = (uint32_t)a.S * 16u;
+  const long long es = p.lin.es, step = (long long)gridDim.x * G;
+  const int L = a.L, n = a.n;
+  const double scale = 1.0 / (double)a.qm;
+  long long item = (long long)blockIdx.x * G + g;
+  if (tid == 0 && item < p.lin.count) {
+    tma_copy(X, p.f + p.lin.base(item), row_bytes, bar_f);
+    tma_copy(Y, p.g + p.lin.base(item), row_bytes, bar_g);
+  }
+  for (; item < p.lin.count; item += step) {
+    const long long base = p.lin.base(item);
+    const long long next = item + step < p.lin.count ? p.lin.base(item + step) : -1;
+    for (int res = 0; res < n; ++res) {
+      const bool last = res == n - 1;
+      const P0Res<SYM_COMPLEX> p0{&a, tb, res};
+      const double2* U = tb + (a.oU + res * a.nu);
+      double2 v[Cfg::E], w[Cfg::E];
+      if (use_tm) tmem_wait_st();  // the previous residue's TMEM stores (accumulator, g stash)
+      mbar_wait(bar_f, ph_f);
+      ph_f ^= 1;
+      load_raw_pp2<Cfg>(v, L, X, tid);
+      if (res == 0 || SPLIT) {
+        mbar_wait(bar_g, ph_g);
+        ph_g ^= 1;
+        load_raw_pp2<Cfg>(w, L, Y, tid);
+        if constexpr (!SPLIT) {
+          if (n > 1) tm_store<E0>(tg, w);
+        }
+        if (res) {
+          twiddle_u_pp2<Cfg, +1>(v, U, tid);
+          twiddle_u_pp2<Cfg, +1>(w, U, tid);
+        }
+      } else {
+        sfor<E0 / 4>([&](auto Ki) HC_INL { tm_ld4(tg + 16 * Ki, w + 4 * Ki); });
+        twiddle_u_pp2<Cfg, +1>(v, U, tid);
+        twiddle_u_pp2<Cfg, +1>(w, U, tid);
+      }
+      sync();  // X and Y consumed before the pair's first exchange overwrites them
+      auto hk = [&]() HC_INL {  // X and Y free: next f (this line's next residue, or the next line)
+        if (tid == 0) {
+          const long long nb = last ? next : base;
+          if (nb >= 0) tma_copy(X, p.f + nb, row_bytes, bar_f);
+          if (last && next >= 0) l2_prefetch(p.g + next, row_bytes);
+        }
+      };
+      if constexpr (SPLIT) {
+        // f's spectrum parks in TMEM while g's last pass runs; the product lands in v
+        auto stash = [&](const double2(&x)[Cfg::E]) HC_INL { tm_store<Cfg::ES>(tf, x); };
+        fft_forward_pair_split<Cfg, GroupSync, P0Res<SYM_COMPLEX>, decltype(hk), decltype(stash)>(v, w, X, Y, mt, tid,
+                                                                                                  sync, p0, hk, stash);
+        tmem_wait_st();
+        sfor<Cfg::ES / 4>([&](auto Ki) HC_INL {
+          double2 F4[4];
+          tm_ld4(tf + 16 * Ki, F4);
+          sfor<4>([&](auto i) HC_INL { v[4 * Ki + i] = cmul(w[4 * Ki + i], F4[i]); });
+        });
+        sync();  // Y read by every thread before the inverse's first exchange
+      } else {
+        fft_forward_pair<Cfg, GroupSync, P0Res<SYM_COMPLEX>, decltype(hk)>(v, w, X, Y, mt, tid, sync, p0, hk);
+        sfor<CL>([&](auto Ci) HC_INL {
+          constexpr int c = Ci;
+          if (bvalid<Cfg, Cfg::P - 1>(c, tid)) sfor<RL>([&](auto Ki) HC_INL { v[c * RL + Ki] = cmul(v[c * RL + Ki], w[c * RL + Ki]); });
+        });
+      }
+      auto hki = [&]() HC_INL {  // Y free: the next line's g (L2-prefetched); SPLIT: this line's again
+        if (tid == 0) {
+          if (last && next >= 0) tma_copy(Y, p.g + next, row_bytes, bar_g);
+          else if (SPLIT && !last) tma_copy(Y, p.g + base, row_bytes, bar_g);
+        }
+      };
+      fft_inverse<Cfg, GroupSync, P0Res<SYM_COMPLEX>, decltype(hki)>(v, Y, mt, tid, sync, p0, hki);
+      if (res) twiddle_u_pp2<Cfg, -1>(v, U, tid);
+      if (res) {
+        sfor<E0 / 4>([&](auto Ki) HC_INL {
+          double2 t4[4];
+          tm_ld4(ta + 16 * Ki, t4);
+          sfor<4>([&](auto i) HC_INL { v[4 * Ki + i] = cadd(v[4 * Ki + i], t4[i]); });
+        });
+      }
+      if (!last) {
+        tm_store<E0>(ta, v);
+      } else {
+        double2* out = p.out + base;
+        sfor<C0>([&](auto Ci) HC_INL {
+          constexpr int c = Ci;
+          const int b = tid + c * T;
+          if (bvalid<Cfg, 0>(c, tid))
+            sfor<R0>([&](auto Ai) HC_INL {
+              const int s = Ns1 * Ai + b;
+              if (s < L) __stcs(out + (long long)s * es, cscale(v[c * R0 + Ai], scale));
+            });
+        });
+      }
+    }
+  }
+  if (use_tm) tmem_wait_st();
+  tmem_fence_before();
+  __syncthreads();
+  if (use_tm && threadIdx.x < 32) tmem_dealloc(tm_base, TL::COLS);
+}
+
 // ------------------------------------------------------------- conv1d, paired --
 // For radix plans with at most 16 values per thread: the forward FFTs of f and g run as one
 // interleaved pair (fft_forward_pair) through two exchange buffers X (f) and Y (g); the product

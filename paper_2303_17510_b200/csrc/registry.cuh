@@ -22,6 +22,8 @@ struct KernelEntry {
   int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
   int xs = 0, stash = 0;           // exchange buffer / shared-memory stash per group (complex)
   bool pair = false;               // conv kernel is k_conv1d_pair (two exchange buffers per group)
+  const void* convpp2_fn = nullptr;  // paired ping-pong variant (k_conv1d_pp2: complex, L <= B)
+  void (*convpp2)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   const void* convpp_fn = nullptr;  // ping-pong variant (k_conv1d_pp)
   void (*convpp)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   // column-tile outer-axis passes (complex / centered only): GC interleaved column groups
@@ -76,6 +78,16 @@ KernelEntry make_entry(const char* radix) {
     if constexpr (PAIR) k_conv1d_pair<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
     else k_conv1d<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
   };
+  // paired ping-pong (complex): kernels that own the SM with at most 16 last-pass values per
+  // thread (B200: 4096-point blocks 0.560 -> 0.484 ms for L = 4000 x 4096 lines; the split
+  // last-pass variant for 16x16x24 spills at 384 threads, 0.79 -> 0.91 ms; the smaller plans,
+  // several CTAs per SM at capped registers, spill too: 2048 0.29 -> 0.35, 512 0.24 -> 0.30 ms)
+  if constexpr (SYM == SYM_COMPLEX && Cfg::ES <= 16 && Cfg::T <= 256 && (2 * Cfg::XS * G * 16 > 116 * 1024)) {
+    e.convpp2_fn = (const void*)k_conv1d_pp2<Cfg, G, MINB>;
+    e.convpp2 = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
+      k_conv1d_pp2<Cfg, G, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
+    };
+  }
   e.convpp_fn = (const void*)k_conv1d_pp<SYM, Cfg, G, SR, MINB>;
   e.convpp = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
     k_conv1d_pp<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);

@@ -147,6 +147,20 @@ def test_conv1d_vs_oracle(cuda, oracle, case):
     np.testing.assert_array_equal(ft.cpu().numpy(), out)
 
 
+@pytest.mark.parametrize("L,M,m,C_", [(4000, 7999, 4096, 300), (4096, 4096, 4096, 150), (4096, 8191, 4096, 149),
+                                       (3001, 6001, 4096, 7), (1, 1, 4096, 3)])
+def test_conv1d_paired_kernel(cuda, oracle, L, M, m, C_):
+    """k_conv1d_pp2 (paired forward FFTs, TMEM accumulator and g stash): more lines than CTAs
+    (persistent loop, next-line copies), n = 1 and n = 2 residues, short lines."""
+    rng = np.random.default_rng(L + C_)
+    f, g = _rand(rng, (C_, L)), _rand(rng, (C_, L))
+    plan = cuda.Conv1dPlan(L, M, m, cuda.Symmetry.Complex, C_=C_)
+    out = cuda.convolve([_t(f), _t(g)], plan.mult, plan, out=_t(f) * 0)[0].cpu().numpy()
+    rows = range(0, C_, max(1, C_ // 12))
+    ref = np.stack([oracle.convolve([(L, M, m, 0)], f[c], g[c]) for c in rows])
+    _check_conv(out[list(rows)], ref, f[list(rows)], g[list(rows)])
+
+
 def test_conv1d_direct_sum_small(cuda, oracle):
     """SPEC.md:414 Fig.1 geometry and SPEC.md:592 [1,2]*[3,4]."""
     plan = cuda.Conv1dPlan(6, 11, 4)
