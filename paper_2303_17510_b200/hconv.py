@@ -522,6 +522,33 @@ def tune_nd(axes: Sequence[AxisSpec], mult: Optional[MultOperator] = None, devic
     return ConvPlanND([AxisSpec(a.L, a.M, None, a.symmetry) for a in axes], mult, device)
 
 
+class CapturedConvolution:
+    """A convolution captured once into a CUDA graph and replayed: the kernels of
+    convolve / convolve_nd on fixed device arrays without the host-side launch path (Python,
+    ctypes, plan bookkeeping) between steps -- what bounds small problems (config 1: 1024 lines
+    of 1024 points take ~40 us on the device, about as long as issuing the call).  The plan's
+    work buffers are allocated by the warm-up call before capture.  Built-in product or native
+    (fn=) operators only: a Python operator cannot be captured."""
+
+    def __init__(self, inputs: Sequence[torch.Tensor], mult: MultOperator, plan: "_Plan", out: Outs = None):
+        if mult.kind != _abi.MULT_PRODUCT and mult.apply is not None:
+            raise ValueError("a Python multiplication operator cannot be captured in a CUDA graph")
+        run = convolve_nd if isinstance(plan, ConvPlanND) else convolve
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.outs = run(inputs, mult, plan, out)  # warm-up: allocates the plan's scratch
+        torch.cuda.current_stream().wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            run(inputs, mult, plan, self.outs)
+        self._keep = (list(inputs), plan)
+
+    def __call__(self) -> list[torch.Tensor]:
+        self.graph.replay()
+        return self.outs
+
+
 def fill_uniform(t: torch.Tensor, seed: int, a: int, first_index: int = 0, stream=None) -> torch.Tensor:
     """Counter-based synthetic inputs written on the device."""
     _dev(t)

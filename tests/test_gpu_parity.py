@@ -161,6 +161,31 @@ def test_conv1d_paired_kernel(cuda, oracle, L, M, m, C_):
     _check_conv(out[list(rows)], ref, f[list(rows)], g[list(rows)])
 
 
+def test_captured_convolution_replays(cuda):
+    """CapturedConvolution (CUDA graph of the API call) gives the direct call's results, and a
+    replay picks up new input values written into the same arrays."""
+    import torch
+
+    for plan, shape in [(cuda.Conv1dPlan(1024, 2047, 2048, C_=64), (64, 1024)),
+                        (cuda.ConvPlanND([cuda.AxisSpec(96, 191, 96), cuda.AxisSpec(80, 159, 48)]), (96, 80))]:
+        f = torch.empty(shape, dtype=torch.complex128, device="cuda")
+        g = torch.empty_like(f)
+        cuda.fill_uniform(f, 3, 0)
+        cuda.fill_uniform(g, 3, 1)
+        run = cuda.convolve_nd if isinstance(plan, cuda.ConvPlanND) else cuda.convolve
+        ref = run([f, g], plan.mult, plan, out=torch.empty_like(f))[0].clone()
+        cap = cuda.CapturedConvolution([f, g], plan.mult, plan, out=torch.empty_like(f))
+        for _ in range(2):
+            h = cap()[0]
+        torch.cuda.synchronize()
+        torch.testing.assert_close(h, ref, rtol=0, atol=0)
+        cuda.fill_uniform(f, 4, 0)
+        ref2 = run([f, g], plan.mult, plan, out=torch.empty_like(f))[0].clone()
+        h2 = cap()[0]
+        torch.cuda.synchronize()
+        torch.testing.assert_close(h2, ref2, rtol=0, atol=0)
+
+
 def test_conv1d_direct_sum_small(cuda, oracle):
     """SPEC.md:414 Fig.1 geometry and SPEC.md:592 [1,2]*[3,4]."""
     plan = cuda.Conv1dPlan(6, 11, 4)
