@@ -437,9 +437,10 @@ int cols_tabn(const AxisPlan& ap) {
   const size_t room = kSmemCap / sizeof(double2) > groups ? kSmemCap / sizeof(double2) - groups : 0;
   return (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
 }
-int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items) {
-  const int nb = occupancy(fn, k->T * k->gc, smem);
-  const long long need = (items + k->gc - 1) / k->gc;
+int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items, int gc = 0) {
+  if (gc == 0) gc = k->gc;
+  const int nb = occupancy(fn, k->T * gc, smem);
+  const long long need = (items + gc - 1) / gc;
   return (int)std::max<long long>(1, std::min(need, (long long)nb * dev_info().sms));
 }
 
@@ -447,8 +448,10 @@ int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items
 // at least the middle-pass tables must fit; returns the staged table prefix (0 = does not fit).
 int cols_pp_tabn(const AxisPlan& ap, int rows, size_t* smem) {
   static const bool off = std::getenv("HCONV_NO_COLS_PP") && std::getenv("HCONV_NO_COLS_PP")[0] == '1';
-  if (off || !ap.k->fwdcp) return 0;
-  const size_t bufs = 2 * (size_t)ap.k->gc * (size_t)std::max(ap.k->xs, rows);
+  // only at the unpipelined kernel's tile width: narrower tiles cost more in DRAM row efficiency
+  // than the pipelining recovers (c4 outer 4096-point columns, 2 -> 1 column per tile: 0.54 -> 0.69 ms)
+  if (off || !ap.k->fwdcp || ap.k->gcp != ap.k->gc) return 0;
+  const size_t bufs = 2 * (size_t)ap.k->gcp * (size_t)std::max(ap.k->xs, rows);
   if ((bufs + (size_t)ap.k->mt) * sizeof(double2) > kSmemCap) return 0;
   const size_t room = kSmemCap / sizeof(double2) - bufs;
   const int tabn = (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
@@ -462,7 +465,7 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
   size_t smpp = 0;
   int tpp = 0;
   if (use_cols(ap, lin) && !ref_order && (tpp = cols_pp_tabn(ap, (int)ap.data, &smpp)) > 0) {
-    const int grid = grid_cols(ap.k->fwdcp_fn, ap.k, smpp, lin.count);
+    const int grid = grid_cols(ap.k->fwdcp_fn, ap.k, smpp, lin.count, ap.k->gcp);
     hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
     a.ax.tabn = tpp;
     ap.k->fwdcp(a, grid, smpp, s);
@@ -494,7 +497,7 @@ void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
   size_t smpp = 0;
   int tpp = 0;
   if (use_cols(ap, lout) && !ref_order && (tpp = cols_pp_tabn(ap, ap.dev.Bc, &smpp)) > 0) {
-    const int grid = grid_cols(ap.k->bwdcp_fn, ap.k, smpp, lin.count);
+    const int grid = grid_cols(ap.k->bwdcp_fn, ap.k, smpp, lin.count, ap.k->gcp);
     hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
     a.ax.tabn = tpp;
     ap.k->bwdcp(a, grid, smpp, s);

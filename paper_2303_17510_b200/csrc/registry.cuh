@@ -27,7 +27,7 @@ struct KernelEntry {
   const void* convpp_fn = nullptr;  // ping-pong variant (k_conv1d_pp)
   void (*convpp)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   // column-tile outer-axis passes (complex / centered only): GC interleaved column groups
-  int gc = 0;
+  int gc = 0, gcp = 0;  // column groups per CTA: unpipelined / pipelined kernels
   const void* fwdc_fn = nullptr;
   const void* bwdc_fn = nullptr;
   void (*fwdc)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
@@ -45,6 +45,14 @@ template <class Cfg>
 constexpr int column_groups() {
   int g = 8;
   while (g > 1 && (g * Cfg::T > 1024 || (long long)g * Cfg::XS * 16 > 200 * 1024)) g /= 2;
+  return g;
+}
+
+// pipelined column tiles: two tile buffers per CTA, so up to half the groups of column_groups
+template <class Cfg>
+constexpr int column_groups_pp() {
+  int g = 8;
+  while (g > 1 && (g * Cfg::T > 1024 || 2LL * g * Cfg::XS * 16 > 200 * 1024)) g /= 2;
   return g;
 }
 
@@ -109,13 +117,15 @@ KernelEntry make_entry(const char* radix) {
     e.bwdc = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
       k_pfft_bwd_cols<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
     };
-    e.fwdcp_fn = (const void*)k_pfft_fwd_cols_pp<SYM, Cfg, GC>;
-    e.bwdcp_fn = (const void*)k_pfft_bwd_cols_pp<SYM, Cfg, GC>;
+    constexpr int GP = column_groups_pp<Cfg>();
+    e.gcp = GP;
+    e.fwdcp_fn = (const void*)k_pfft_fwd_cols_pp<SYM, Cfg, GP>;
+    e.bwdcp_fn = (const void*)k_pfft_bwd_cols_pp<SYM, Cfg, GP>;
     e.fwdcp = [](const FwdArgs& a, int grid, size_t sm, cudaStream_t s) {
-      k_pfft_fwd_cols_pp<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+      k_pfft_fwd_cols_pp<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a);
     };
     e.bwdcp = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
-      k_pfft_bwd_cols_pp<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a);
+      k_pfft_bwd_cols_pp<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a);
     };
   }
   return e;
