@@ -1159,6 +1159,11 @@ __global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
 }
 
 // --------------------------------------------------------- column-tile pfft --
+// HC_COLS_PREFETCH=1: every round first warms L2 with the rows of its column for the next round
+// (one 16-byte bulk prefetch per row: measured slower, c4 0.51 -> 0.66 ms, so off)
+#ifndef HC_COLS_PREFETCH
+#define HC_COLS_PREFETCH 0
+#endif
 // Outer-axis passes of the N-D driver read columns at a large element stride.  Here the GC
 // line groups of a CTA take GC ADJACENT columns and interleave thread by thread (thread t ->
 // group t % GC), so every load/store instruction of a warp touches GC consecutive columns
@@ -1182,6 +1187,14 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols(FwdArgs p) {
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
     const bool live = item < p.lin.count;
+    // warm L2 with this column's rows of the next round (HBM latency overlaps this round)
+    if (HC_COLS_PREFETCH) {
+      const long long nitem = item + (long long)gridDim.x * GC;
+      if (nitem < p.lin.count) {
+        const double2* src = p.f + p.lin.base(nitem);
+        for (int j = tid; j < a.S; j += T) l2_prefetch(src + (long long)j * p.lin.es, 16);
+      }
+    }
     double2 v[Cfg::E];
     if (live) load_pass0<SYM, Cfg>(v, a, tp, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X, mt, tid, sync, p0);
@@ -1218,6 +1231,13 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
     const bool live = item < p.lin.count;
+    if (HC_COLS_PREFETCH) {
+      const long long nitem = item + (long long)gridDim.x * GC;
+      if (nitem < p.lin.count) {
+        const double2* src = (const double2*)p.F + p.lin.base(nitem);
+        for (int j = tid; j < Cfg::N; j += T) l2_prefetch(src + (long long)j * p.lin.es, 16);
+      }
+    }
     double2 v[Cfg::E];
     if (live) {
       const long long ib = p.lin.base(item), ies = p.lin.es;
