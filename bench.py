@@ -152,6 +152,11 @@ def launches_per_step(params):
     return params[0].n * (A + inner + 1)
 
 
+# candidate subtransform sizes of the CPU baseline's own tuning probe (hybrid, explicit, pow2)
+CPU_CANDIDATES = {"c1": [256, 512, 1024, 2048], "c2": [1024, 1536, 2000, 2048, 3000, 3072, 4096, 6000, 6144, 12000],
+                  "c3": [2048, 4096, 8192, 12288]}
+
+
 class CpuArm:
     """Oracle (CPU restatement, TEST INFRASTRUCTURE) on a bounded sample of the 1D workload:
     a probe sizes the sample, then each call convolves `rows` copies of the batch."""
@@ -168,10 +173,22 @@ class CpuArm:
             raise SystemExit("CPU baseline is timed on the 1D configs (N-D: tools/bench_all.py)")
         self.L, self.M, self.s = axes[0]
         self.S = shape[0]
-        self.m = m or {"c1": 1024, "c2": 1024, "c3": 8192}[name]  # default: the GPU planner's usual choice
         probe = max(self.threads, 8)
         self.rows = probe
-        self.per_row = self.run()[1] / probe
+        if m:
+            self.m = m
+            self.per_row = self.run()[1] / probe
+        else:
+            # the CPU path's own hybrid choice: time a probe of each candidate m (the paper's tuner,
+            # PAPER.md:894-914, on the host cores) and keep the fastest
+            best = None
+            for mc in CPU_CANDIDATES[name]:
+                self.m = mc
+                dt = self.run()[1]
+                if best is None or dt < best[1]:
+                    best = (mc, dt)
+            self.m = best[0]
+            self.per_row = best[1] / probe
 
     def size_for(self, seconds):
         self.rows = int(min(self.C, max(self.threads, seconds / max(self.per_row, 1e-9))))
@@ -411,7 +428,7 @@ def run_cuda(args):
     }
     if world == 1 and not args.no_cpu:
         try:
-            arm = CpuArm(name, params[0].m)
+            arm = CpuArm(name)  # the CPU path's own tuned m (the GPU plan's m may not suit the CPU)
             arm.size_for(15.0)
             v, dt = arm.run()
             line["cpu_baseline"] = {"value": v, "unit": "points/s", "cores": arm.threads, "kind": "port",
