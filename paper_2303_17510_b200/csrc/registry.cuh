@@ -159,6 +159,13 @@ KernelEntry make_naive_entry() {
 #ifndef HC_R512_MINB
 #define HC_R512_MINB 8
 #endif
+// (1024-point plan: G = 1 with 5 CTAs per SM measured no faster for c1, 0.0466 vs 0.0457 ms)
+#ifndef HC_R1024_G
+#define HC_R1024_G 2
+#endif
+#ifndef HC_R1024_MINB
+#define HC_R1024_MINB 1
+#endif
 // Radix plans (complex FFT length -> passes, threads per line group, groups per CTA).
 template <int SYM>
 inline void build_registry(KernelEntry* out, int* count) {
@@ -168,7 +175,7 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, 2>("16x16x4");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, HC_R1024_G, false, HC_R1024_MINB>("16x16x4");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1, true, 3>("16x16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
