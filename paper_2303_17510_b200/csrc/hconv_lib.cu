@@ -1366,18 +1366,26 @@ hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* con
       int slot = 0;
       for (long long c0 = 0; c0 < C; c0 += per, slot = (slot + 1) % HostPipe::kSlots) {
         const long long cnt = std::min(per, C - c0);
-        const size_t bytes = (size_t)((cnt - 1) * dist + S) * sizeof(double2);
         const size_t off = (size_t)(c0 * dist) * sizeof(double2);
         double2* const* b = hp.buf[slot].data();
         // slot reuse: its previous chunk has been copied back
         CK(cudaStreamWaitEvent(hp.st[0], hp.drained[slot], 0));
-        for (size_t a = 0; a < A; ++a) CK(cudaMemcpyAsync(b[a], hin(a) + off, bytes, cudaMemcpyHostToDevice, hp.st[0]));
+        // rows only (the gaps between rows at distance dist are neither read nor written)
+        const size_t pitch = (size_t)dist * sizeof(double2), width = (size_t)S * sizeof(double2);
+        const bool rows = dist != S;
+        for (size_t a = 0; a < A; ++a) {
+          if (rows) CK(cudaMemcpy2DAsync(b[a], pitch, hin(a) + off, pitch, width, (size_t)cnt, cudaMemcpyHostToDevice, hp.st[0]));
+          else CK(cudaMemcpyAsync(b[a], hin(a) + off, width * (size_t)cnt, cudaMemcpyHostToDevice, hp.st[0]));
+        }
         CK(cudaEventRecord(hp.loaded[slot], hp.st[0]));
         CK(cudaStreamWaitEvent(hp.st[1], hp.loaded[slot], 0));
         conv1d(p, ap, cnt, dist, b, b, hp.st[1]);  // in place: outputs in the first B buffers
         CK(cudaEventRecord(hp.done[slot], hp.st[1]));
         CK(cudaStreamWaitEvent(hp.st[2], hp.done[slot], 0));
-        for (size_t o = 0; o < Bo; ++o) CK(cudaMemcpyAsync(hout(o) + off, b[o], bytes, cudaMemcpyDeviceToHost, hp.st[2]));
+        for (size_t o = 0; o < Bo; ++o) {
+          if (rows) CK(cudaMemcpy2DAsync(hout(o) + off, pitch, b[o], pitch, width, (size_t)cnt, cudaMemcpyDeviceToHost, hp.st[2]));
+          else CK(cudaMemcpyAsync(hout(o) + off, b[o], width * (size_t)cnt, cudaMemcpyDeviceToHost, hp.st[2]));
+        }
         CK(cudaEventRecord(hp.drained[slot], hp.st[2]));
       }
       CK(cudaStreamSynchronize(hp.st[2]));

@@ -186,6 +186,42 @@ def test_captured_convolution_replays(cuda):
         torch.testing.assert_close(h2, ref2, rtol=0, atol=0)
 
 
+@pytest.mark.parametrize("L,M,m,sym", [(6000, 11999, 6144, 0), (4000, 7999, 4096, 0), (1024, 2047, 1024, 0),
+                                       (16383, 24574, 8192, 2), (511, 766, 256, 1)])
+def test_conv1d_row_distance(cuda, oracle, L, M, m, sym):
+    """Copies at a row distance larger than the stored length (the ABI's `dist`): every kernel
+    family reads and writes only its rows and leaves the gaps untouched, on the device and through
+    the host-buffer entry point."""
+    import torch
+
+    S = (L + 1) // 2 if sym == 2 else L
+    C_, gap = 5, 7
+    dist = S + gap
+    rng = np.random.default_rng(L)
+    f, g = _rand(rng, (C_, dist)), _rand(rng, (C_, dist))
+    if sym == 2:
+        f[:, 0], g[:, 0] = f[:, 0].real, g[:, 0].real
+    plan = cuda.Conv1dPlan(L, M, m, cuda.Symmetry(sym), C_=C_, dist=dist)
+    sentinel = 1234.5 - 6.5j
+    out = np.full((C_, dist), sentinel)
+    ot = _t(out)
+    cuda.convolve([_t(f), _t(g)], plan.mult, plan, out=ot)
+    h = ot.cpu().numpy()
+    ref = np.stack([oracle.convolve([(L, M, m, sym)], f[c, :S], g[c, :S]) for c in range(C_)])
+    _check_conv(h[:, :S], ref, f[:, :S], g[:, :S])
+    assert np.all(h[:, S:] == sentinel)
+    for chunks in ("8", "2"):  # one row per chunk, and several rows (gaps inside a chunk)
+        import os
+
+        os.environ["HCONV_HOST_CHUNKS"] = chunks
+        try:
+            oh = torch.from_numpy(out.copy())
+            cuda.convolve_host([torch.from_numpy(f), torch.from_numpy(g)], plan.mult, plan, out=oh)
+        finally:
+            del os.environ["HCONV_HOST_CHUNKS"]
+        np.testing.assert_array_equal(oh.numpy(), h)
+
+
 def test_conv1d_direct_sum_small(cuda, oracle):
     """SPEC.md:414 Fig.1 geometry and SPEC.md:592 [1,2]*[3,4]."""
     plan = cuda.Conv1dPlan(6, 11, 4)
