@@ -159,6 +159,12 @@ KernelEntry make_naive_entry() {
 #ifndef HC_R512_MINB
 #define HC_R512_MINB 8
 #endif
+#ifndef HC_R4096_MINB
+#define HC_R4096_MINB 1
+#endif
+#ifndef HC_R4096_SMEM_STASH
+#define HC_R4096_SMEM_STASH false
+#endif
 // (1024-point plan: G = 1 with 5 CTAs per SM measured no faster for c1, 0.0466 vs 0.0457 ms)
 #ifndef HC_R1024_G
 #define HC_R1024_G 2
@@ -179,7 +185,7 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1, true, 3>("16x16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1>("16x16x16");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
   // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
   out[k++] = make_naive_entry<SYM>();
