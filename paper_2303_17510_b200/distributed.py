@@ -11,7 +11,9 @@ axis after one all-to-all transpose:
   for each residue block r of the y axis (PAPER.md:584-600 with y as the outer axis):
     1. local forward padded y-FFT of the A inputs, ONE strided launch per input
        (hconv_pfft_forward_lines), written k-major: F_a[k][x][z], so the k-block destined for
-       rank h is one contiguous run (the all-to-all send buffer needs no packing)
+       rank h is one contiguous run (the all-to-all send buffer needs no packing); each input's
+       exchange is issued asynchronously, so it overlaps the next input's forward (and each
+       output's exchange the previous output's backward)
     2. all-to-all: rank g receives the spectral y-lines k in [k0_g, k1_g) of every x-slab,
        [h][k][x_h][z], and places them as T_a[k][x][z] with x complete (G slice copies)
     3. the (d-1)-D subconvolutions of all nk spectral lines in ONE batched call
@@ -137,10 +139,11 @@ def cuda_backend(device: Optional[torch.device] = None) -> Backend:
     return Backend(hconv.lib(), dev, lambda: C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
 
 
-def _a2a(recv: torch.Tensor, send: torch.Tensor, rsplit: list[int], ssplit: list[int], group) -> None:
-    """all_to_all_single on complex data (exchanged as float64 pairs)."""
-    dist.all_to_all_single(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
-                           [2 * s for s in rsplit], [2 * s for s in ssplit], group=group)
+def _a2a(recv: torch.Tensor, send: torch.Tensor, rsplit: list[int], ssplit: list[int], group, async_op=False):
+    """all_to_all_single on complex data (exchanged as float64 pairs); async_op returns the work
+    handle (NCCL: the exchange runs on NCCL's stream, work.wait() orders the current stream)."""
+    return dist.all_to_all_single(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
+                                  [2 * s for s in rsplit], [2 * s for s in ssplit], group=group, async_op=async_op)
 
 
 @dataclass
@@ -213,11 +216,13 @@ class SlabConvND:
         lspec = _lines(nxz, nxz, 0, 1, nxz)       # the same lines k-major: F[k][x][z]
         send_sizes = [(b - a) * nxz for a, b in self.ks]
         recv_sizes = [nk * (b - a) * Z for a, b in self.xs]
-        F = torch.empty(By * nxz, dtype=dt, device=dev)
-        recv = torch.empty(sum(recv_sizes), dtype=dt, device=dev)
+        # one spectral / exchange buffer per input and per output: each exchange runs
+        # asynchronously while the next input's forward (or the previous output's backward) computes
+        F = [torch.empty(By * nxz, dtype=dt, device=dev) for _ in range(self.A)]
+        recv = [torch.empty(sum(recv_sizes), dtype=dt, device=dev) for _ in range(self.A)]
         T = [torch.empty(max(1, nk) * Lx * Z, dtype=dt, device=dev) for _ in range(max(self.A, self.B))]
-        back = torch.empty(sum(recv_sizes), dtype=dt, device=dev)
-        W = torch.empty(By * nxz, dtype=dt, device=dev)
+        back = [torch.empty(sum(recv_sizes), dtype=dt, device=dev) for _ in range(self.B)]
+        W = [torch.empty(By * nxz, dtype=dt, device=dev) for _ in range(self.B)]
         # results accumulate in separate buffers when an output aliases an input (inputs are
         # read by every residue's forward)
         ins_ptrs = {t.data_ptr() for t in inputs}
@@ -225,27 +230,34 @@ class SlabConvND:
         n_res = self.py.n
         scale = 1.0 / (self.py.q * self.py.m)
         for r in range(n_res):
+            works = []
             for a in range(self.A):
-                self.b.forward_lines(inputs[a], self.py, r, lin, F, lspec)
-                _a2a(recv, F, recv_sizes, send_sizes, self.group)
+                self.b.forward_lines(inputs[a], self.py, r, lin, F[a], lspec)
+                works.append(_a2a(recv[a], F[a], recv_sizes, send_sizes, self.group, async_op=True))
+            for a in range(self.A):
+                works[a].wait()
                 Ta = T[a].view(max(1, nk), Lx, Z)
                 off = 0
                 for (xa, xb), sz in zip(self.xs, recv_sizes):
                     if sz:
-                        Ta[:, xa:xb, :] = recv[off:off + sz].view(nk, xb - xa, Z)
+                        Ta[:, xa:xb, :] = recv[a][off:off + sz].view(nk, xb - xa, Z)
                     off += sz
             if nk:
                 self.inner_plan.convolve(T[:self.A], T[:self.B])
             last = r == n_res - 1
+            works = []
             for b in range(self.B):
                 Tb = T[b].view(max(1, nk), Lx, Z)
                 off = 0
                 for (xa, xb), sz in zip(self.xs, recv_sizes):
                     if sz:
-                        back[off:off + sz].view(nk, xb - xa, Z).copy_(Tb[:, xa:xb, :])
+                        back[b][off:off + sz].view(nk, xb - xa, Z).copy_(Tb[:, xa:xb, :])
                     off += sz
-                _a2a(W, back, send_sizes, recv_sizes, self.group)
-                self.b.backward_lines(W, self.py, r, lspec, acc[b], lin, accumulate=r > 0, scale=scale if last else 1.0)
+                works.append(_a2a(W[b], back[b], send_sizes, recv_sizes, self.group, async_op=True))
+            for b in range(self.B):
+                works[b].wait()
+                self.b.backward_lines(W[b], self.py, r, lspec, acc[b], lin, accumulate=r > 0,
+                                      scale=scale if last else 1.0)
         for o, a_ in zip(outs, acc):
             if o.data_ptr() != a_.data_ptr():
                 o.copy_(a_)
