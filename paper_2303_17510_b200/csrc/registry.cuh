@@ -159,6 +159,9 @@ KernelEntry make_naive_entry() {
 #ifndef HC_R512_MINB
 #define HC_R512_MINB 8
 #endif
+#ifndef HC_R6144_PLAN
+#define HC_R6144_PLAN 1
+#endif
 #ifndef HC_R4096_MINB
 #define HC_R4096_MINB 1
 #endif
@@ -187,7 +190,11 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
   // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
+#if HC_R6144_PLAN == 2
+  out[k++] = make_entry<SYM, FFTCfg<Radices<24, 16, 16>, 256>, 1>("24x16x16");
+#else
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
+#endif
   out[k++] = make_naive_entry<SYM>();
   *count = k;
 }
