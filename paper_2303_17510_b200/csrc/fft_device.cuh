@@ -165,6 +165,98 @@ struct DFT<4, DIR> {
   }
 };
 
+#ifndef HC_DFT_FMA
+#define HC_DFT_FMA 1
+#endif
+#if HC_DFT_FMA
+// Hand-scheduled 8- and 16-point DFTs: the four-step form of the generic template, with every
+// non-trivial internal twiddle written as c (1 + i DIR t) (t = tan of the angle) or
+// sqrt(1/2) (+-1 + i DIR) and its scale c folded into the FMAs of the following radix-4 / radix-2
+// butterflies (the ratio of two scales is again a tangent, c3/c1 = tan(pi/8)).  DFT16: 144 FP64
+// instructions instead of 160; DFT8: 52 instead of 56.  Natural-order output, same as DFT<R>.
+namespace dftc {
+constexpr double h = 0.70710678118654752440084436210484903928;   // sqrt(1/2)
+constexpr double c1 = 0.92387953251128675612818318939678828682;  // cos(pi/8)
+constexpr double c3 = 0.38268343236508977172845998403039886676;  // cos(3pi/8)
+constexpr double t1 = 0.41421356237309504880168872420969807857;  // tan(pi/8) = c3/c1
+constexpr double t3 = 2.41421356237309504880168872420969807857;  // tan(3pi/8) = c1/c3
+}  // namespace dftc
+// y (1 + i DIR t)
+template <int DIR>
+__device__ __forceinline__ double2 tan_rot(double2 y, double t) {
+  return make_double2(fma(-DIR * t, y.y, y.x), fma(DIR * t, y.x, y.y));
+}
+// a + s b, componentwise
+__device__ __forceinline__ double2 cfma(double s, double2 b, double2 a) { return make_double2(fma(s, b.x, a.x), fma(s, b.y, a.y)); }
+
+template <int DIR>
+struct DFT<16, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    using namespace dftc;
+    double2 y[4][4];  // y[b][ka]: DFT4 over a of x[4a + b]
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      double2 q[4] = {x[b], x[4 + b], x[8 + b], x[12 + b]};
+      DFT<4, DIR>::run(q);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) y[b][k] = q[k];
+    }
+    {  // ka = 0: no twiddles
+      double2 z[4] = {y[0][0], y[1][0], y[2][0], y[3][0]};
+      DFT<4, DIR>::run(z);
+      x[0] = z[0], x[4] = z[1], x[8] = z[2], x[12] = z[3];
+    }
+    {  // ka = 1: zeta^1 = c1 (1 + i DIR t1), zeta^2 = h (1 + i DIR), zeta^3 = c3 (1 + i DIR t3)
+      const double2 u1 = tan_rot<DIR>(y[1][1], t1), u2 = tan_rot<DIR>(y[2][1], 1.0), u3 = tan_rot<DIR>(y[3][1], t3);
+      const double2 s02 = cfma(h, u2, y[0][1]), d02 = cfma(-h, u2, y[0][1]);
+      const double2 p = cfma(t1, u3, u1), q = cfma(-t1, u3, u1);  // (z1 +- z3) / c1
+      const double2 rq = mul_i<DIR>(q);
+      x[1] = cfma(c1, p, s02), x[9] = cfma(-c1, p, s02);
+      x[5] = cfma(c1, rq, d02), x[13] = cfma(-c1, rq, d02);
+    }
+    {  // ka = 2: zeta^2 = h (1 + i DIR), zeta^4 = i^DIR, zeta^6 = h (-1 + i DIR)
+      const double2 v1 = tan_rot<DIR>(y[1][2], 1.0);
+      const double2 w = y[3][2];
+      const double2 v3 = make_double2(-w.x - DIR * w.y, -w.y + DIR * w.x);
+      const double2 r2 = mul_i<DIR>(y[2][2]);
+      const double2 s02 = cadd(y[0][2], r2), d02 = csub(y[0][2], r2);
+      const double2 p = cadd(v1, v3), q = csub(v1, v3);
+      const double2 rq = mul_i<DIR>(q);
+      x[2] = cfma(h, p, s02), x[10] = cfma(-h, p, s02);
+      x[6] = cfma(h, rq, d02), x[14] = cfma(-h, rq, d02);
+    }
+    {  // ka = 3: zeta^3 = c3 (1 + i DIR t3), zeta^6 = h (-1 + i DIR), zeta^9 = -c1 (1 + i DIR t1)
+      const double2 w1 = tan_rot<DIR>(y[1][3], t3), w3 = tan_rot<DIR>(y[3][3], t1);
+      const double2 g = y[2][3];
+      const double2 w2 = make_double2(-g.x - DIR * g.y, -g.y + DIR * g.x);
+      const double2 s02 = cfma(h, w2, y[0][3]), d02 = cfma(-h, w2, y[0][3]);
+      const double2 p = cfma(-t3, w3, w1), q = cfma(t3, w3, w1);  // (z1 +- z3) / c3
+      const double2 rq = mul_i<DIR>(q);
+      x[3] = cfma(c3, p, s02), x[11] = cfma(-c3, p, s02);
+      x[7] = cfma(c3, rq, d02), x[15] = cfma(-c3, rq, d02);
+    }
+  }
+};
+
+template <int DIR>
+struct DFT<8, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    using namespace dftc;
+    double2 y0[4] = {x[0], x[2], x[4], x[6]}, y1[4] = {x[1], x[3], x[5], x[7]};  // DFT4 over a of x[2a + b]
+    DFT<4, DIR>::run(y0);
+    DFT<4, DIR>::run(y1);
+    x[0] = cadd(y0[0], y1[0]), x[4] = csub(y0[0], y1[0]);
+    const double2 u1 = tan_rot<DIR>(y1[1], 1.0);  // zeta8^1 = h (1 + i DIR)
+    x[1] = cfma(h, u1, y0[1]), x[5] = cfma(-h, u1, y0[1]);
+    const double2 r2 = mul_i<DIR>(y1[2]);         // zeta8^2 = i^DIR
+    x[2] = cadd(y0[2], r2), x[6] = csub(y0[2], r2);
+    const double2 w = y1[3];                       // zeta8^3 = h (-1 + i DIR)
+    const double2 u3 = make_double2(-w.x - DIR * w.y, -w.y + DIR * w.x);
+    x[3] = cfma(h, u3, y0[3]), x[7] = cfma(-h, u3, y0[3]);
+  }
+};
+#endif
+
 // ---------------------------------------------------------------- block FFT --
 template <int... Rs>
 struct Radices {
