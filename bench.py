@@ -109,7 +109,15 @@ class ClockSampler:
                                        str(self.gpu), "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
         except OSError:
             self.p = None
-        time.sleep(0.3)
+        # nvidia-smi's first start on a fresh box can take seconds (NVML init): wait for its first
+        # sample so that its start-up does not fall inside the timed region
+        t0 = time.time()
+        while self.p and time.time() - t0 < 10.0:
+            self.f.flush()
+            if Path(self.f.name).stat().st_size > 0:
+                break
+            time.sleep(0.05)
+        time.sleep(0.2)
         return self
 
     def __exit__(self, *exc):
