@@ -255,6 +255,51 @@ struct DFT<8, DIR> {
     x[3] = cfma(h, u3, y0[3]), x[7] = cfma(-h, u3, y0[3]);
   }
 };
+
+// 24 = 8 x 3: the radix-3 butterflies of the second stage take both twiddled inputs in tangent
+// form, z1 = c1 u1 and z2 = c2 u2 (u = y (1 + i tan)), with c1 factored out of the butterfly
+// (r = c2 / c1 inside, c1 folded into the output FMAs): 16 FP64 instructions instead of 22 per
+// group whose two twiddles are both non-trivial (ka = 1, 2, 4, 5, 7); the other groups as before.
+template <int DIR, int KA>
+__device__ __forceinline__ void dft3_tw24(double2 z0, double2 y1, double2 y2, double2* out) {
+  constexpr int e1 = KA % 24, e2 = (2 * KA) % 24;
+  constexpr bool triv1 = e1 % 6 == 0, triv2 = e2 % 6 == 0;
+  if constexpr (!triv1 && !triv2) {
+    constexpr double ca = TwC<24>::c[e1], sa = DIR * TwC<24>::s[e1];
+    constexpr double cb = TwC<24>::c[e2], sb = DIR * TwC<24>::s[e2];
+    constexpr double ta = sa / ca, tb = sb / cb, r = cb / ca;
+    const double2 u1 = make_double2(fma(-ta, y1.y, y1.x), fma(ta, y1.x, y1.y));
+    const double2 u2 = make_double2(fma(-tb, y2.y, y2.x), fma(tb, y2.x, y2.y));
+    const double2 p = cfma(r, u2, u1), q = cfma(-r, u2, u1);  // (z1 + z2) / ca, (z1 - z2) / ca
+    constexpr double k3 = DIR * 0.86602540378443864676 * ca;   // i DIR sin(2pi/3) ca
+    const double2 t2 = cfma(-0.5 * ca, p, z0);
+    out[0] = cfma(ca, p, z0);
+    out[8] = make_double2(fma(-k3, q.y, t2.x), fma(k3, q.x, t2.y));
+    out[16] = make_double2(fma(k3, q.y, t2.x), fma(-k3, q.x, t2.y));
+  } else {
+    double2 z[3] = {z0, twc<24, e1, DIR>(y1), twc<24, e2, DIR>(y2)};
+    DFT<3, DIR>::run(z);
+    out[0] = z[0], out[8] = z[1], out[16] = z[2];
+  }
+}
+
+template <int DIR>
+struct DFT<24, DIR> {
+  static __device__ __forceinline__ void run(double2* x) {
+    double2 y[3][8];  // y[b][ka]: DFT8 over a of x[3a + b]
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      double2 q[8] = {x[b], x[3 + b], x[6 + b], x[9 + b], x[12 + b], x[15 + b], x[18 + b], x[21 + b]};
+      DFT<8, DIR>::run(q);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) y[b][k] = q[k];
+    }
+    sfor<8>([&](auto K) HC_INL {
+      constexpr int ka = K;
+      dft3_tw24<DIR, ka>(y[0][ka], y[1][ka], y[2][ka], x + ka);
+    });
+  }
+};
 #endif
 
 // ---------------------------------------------------------------- block FFT --
