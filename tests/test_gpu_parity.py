@@ -466,3 +466,24 @@ def test_errors(cuda):
     a = torch.zeros(2, 8, dtype=torch.complex128, device="cuda")
     with pytest.raises(ValueError):
         cuda.convolve([a], cuda.builtin_mult_product(2), plan)
+
+
+@pytest.mark.parametrize("L,M,m,sym,C_", [(1, 1, 1, 0, 1), (1, 1, 1, 2, 3), (2, 3, 2, 1, 2), (8, 15, 8, 0, 300000),
+                                           (3, 5, 1, 0, 70000), (6000, 11999, 6144, 0, 1), (16383, 24574, 8192, 2, 1),
+                                           (100, 199, 1000, 0, 5), (7, 13, 64, 2, 9)])
+def test_conv1d_edge_shapes(cuda, oracle, L, M, m, sym, C_):
+    """Edge shapes: single-point lines, tiny lines in huge batches (grid and scratch sizing), one
+    long line, m > M (explicit padding beyond M, SPEC.md:437 'padding beyond M is fine')."""
+    S = (L + 1) // 2 if sym == 2 else L
+    rng = np.random.default_rng(C_ + L)
+    f, g = _rand(rng, (C_, S)), _rand(rng, (C_, S))
+    if sym == 2:
+        f[:, 0], g[:, 0] = f[:, 0].real, g[:, 0].real
+    try:
+        plan = cuda.Conv1dPlan(L, M, m, cuda.Symmetry(sym), C_=C_)
+    except NotImplementedError:
+        pytest.skip("no kernel for this block")
+    out = cuda.convolve([_t(f), _t(g)], plan.mult, plan, out=_t(f) * 0)[0].cpu().numpy()
+    rows = sorted(set(list(range(min(C_, 3))) + [C_ - 1, C_ // 2]))
+    ref = np.stack([oracle.convolve([(L, M, m, sym)], f[c], g[c]) for c in rows])
+    _check_conv(out[rows], ref, f[rows], g[rows])
