@@ -132,19 +132,18 @@ def cmd_verify(args) -> int:
             Ms = sorted({2 * L - 1 if L > 1 else 1, 2 * L}) if kind == 0 else [max(L, math.ceil(3 * L / 2))]
             for M in Ms:
                 for m in sorted({1, max(1, L // 2), L, M}):
-                    axes = [(L, M, m, kind)] * args.dims
-                    shape = [_stored(L, kind if k == args.dims - 1 else (1 if kind == 2 else kind))
-                             for k in range(args.dims)]
+                    # per-axis kinds: a Hermitian array's outer axes are centered
+                    kk = [kind if k == args.dims - 1 else (1 if kind == 2 else kind) for k in range(args.dims)]
+                    shape = [_stored(L, s) for s in kk]
                     x = rng.uniform(-1, 1, shape) + 1j * rng.uniform(-1, 1, shape)
                     y = rng.uniform(-1, 1, shape) + 1j * rng.uniform(-1, 1, shape)
-                    kk = [kind if k == args.dims - 1 else (1 if kind == 2 else kind) for k in range(args.dims)]
                     xt, yt = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
                     if kind == 2:
-                        hconv.hermitian_symmetrize_boundary(xt, [L] * args.dims) if args.dims > 1 else None
-                        hconv.hermitian_symmetrize_boundary(yt, [L] * args.dims) if args.dims > 1 else None
-                        if args.dims == 1:
-                            xt[0] = xt[0].real.to(xt.dtype)
-                            yt[0] = yt[0].real.to(yt.dtype)
+                        for t in (xt, yt):
+                            if args.dims > 1:
+                                hconv.hermitian_symmetrize_boundary(t, [L] * args.dims)
+                            else:
+                                t[0] = t[0].real.to(t.dtype)
                         x, y = xt.cpu().numpy(), yt.cpu().numpy()
                     try:
                         if args.dims == 1:
@@ -260,11 +259,13 @@ def cmd_bench(args) -> int:
 
 
 def _has_kernel(hconv, L, M, m, kind) -> bool:
+    """m is an explicit size (q = 1: one residue block covers the whole padded length) with a
+    radix kernel (direct sums only for blocks of at most 64 points)."""
     try:
         p = hconv.deriveParams(L, M, m, hconv.Symmetry(kind))
     except ValueError:
         return False
-    if p.q != 1 and not (kind != 0 and p.q == 1):
+    if p.q != 1:
         return False
     try:
         plan = hconv.Conv1dPlan(L, M, m, hconv.Symmetry(kind), C_=1)
