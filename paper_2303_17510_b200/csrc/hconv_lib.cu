@@ -638,6 +638,9 @@ std::map<std::string, std::vector<Candidate>>& ranked_memo() {
 }
 
 // tune_1d on the device: median of 5 timed runs after one warm-up, CUDA events.
+// The candidates are timed with the fused binary-product convolution; for a general operator
+// (whose residue loop runs the same padded FFTs through work blocks) that timing is the proxy,
+// while tune_nd times the plan's own operator.
 size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanReport* rep) {
   auto& cache = planner_cache();
   const std::string key = plan_cache_key(sym, L, M, lines);
