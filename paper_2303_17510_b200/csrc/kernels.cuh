@@ -186,10 +186,18 @@ __device__ __forceinline__ void stage_tables(double2* tb, const AxisDev& a, int 
 // accumulator are brought on chip by TMA bulk copies issued one phase ahead -- the next line
 // copy starts as soon as the previous transform has released the exchange buffer, so the
 // HBM/L2 latency overlaps the butterflies of the current transform.
+// HC_CONV_TMEM=1: the register stash of the first spectrum (STASH_REGS) lives in tensor memory
+// instead (frees Cfg::ES complex registers per thread; 128 columns per CTA at most)
+#ifndef HC_CONV_TMEM
+#define HC_CONV_TMEM 1
+#endif
 template <int SYM, class Cfg, int G, bool STASH_REGS, int MINB = 1>
 __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
   extern __shared__ __align__(16) double2 smem[];
   __shared__ __align__(8) uint64_t bars[2 * G];
+  __shared__ uint32_t tm_base;
+  using TLc = TmemLayout<Cfg::T * G, Cfg::ES, 0>;
+  constexpr bool TMST = HC_CONV_TMEM && STASH_REGS && TLc::FITS && TLc::COLS <= 128;
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   double2* tb = smem;
@@ -210,7 +218,14 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
     mbar_init(bar_acc, 1);
     fence_mbar_init();
   }
+  if constexpr (TMST) {
+    if (threadIdx.x < 32) tmem_alloc(&tm_base, TLc::COLS);
+    tmem_fence_before();
+    __syncthreads();
+    tmem_fence_after();
+  }
   sync();
+  const uint32_t tf = TMST ? TLc::f_addr(tm_base) : 0u;
   uint32_t ph_in = 0, ph_acc = 0;
   const uint32_t row_bytes = (uint32_t)a.S * 16u;
   const long long es = p.lin.es, step = (long long)gridDim.x * G;
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       // next f line: the same line for the next residue, else the next item's line
       const double2* fnext = !last ? p.f + base : (item + step < p.lin.count ? p.f + p.lin.base(item + step) : nullptr);
       double2 v[Cfg::E];
-      double2 Fr[STASH_REGS ? Cfg::E : 1];
+      double2 Fr[STASH_REGS && !TMST ? Cfg::E : 1];
       const P0Res<SYM> p0{&a, tp, res};
       // ---- forward padded FFTs of the A = 2 inputs (one code copy: keeps the kernel inside
       //      the instruction cache); input 0 is stashed, input 1 multiplied by it
@@ -266,13 +281,29 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
         });
         HC_TRACE();
         if (inp == 0) {
-          sfor<CL>([&](auto Ci) HC_INL {
-            constexpr int c = Ci;
-            if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-              sfor<RL>([&](auto Ki) HC_INL {
-                if constexpr (STASH_REGS) Fr[c * RL + Ki] = v[c * RL + Ki];
-                else stash[Ki * NBL + tid + c * T] = v[c * RL + Ki];
-              });
+          if constexpr (TMST) {
+            tm_store<Cfg::ES>(tf, v);
+          } else {
+            sfor<CL>([&](auto Ci) HC_INL {
+              constexpr int c = Ci;
+              if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+                sfor<RL>([&](auto Ki) HC_INL {
+                  if constexpr (STASH_REGS) Fr[c * RL + Ki] = v[c * RL + Ki];
+                  else stash[Ki * NBL + tid + c * T] = v[c * RL + Ki];
+                });
+            });
+          }
+        } else if constexpr (TMST) {
+          tmem_wait_st();
+          sfor<Cfg::ES / 4>([&](auto Ki) HC_INL {
+            double2 F4[4];
+            tm_ld4(tf + 16 * Ki, F4);
+            sfor<4>([&](auto i) HC_INL {
+              double2& G_ = v[4 * Ki + i];
+              const double2 F = F4[i];
+              if constexpr (SYM == SYM_HERMITIAN) G_ = make_double2(G_.x * F.x, G_.y * F.y);
+              else G_ = cmul(G_, F);
+            });
           });
         } else {
           sfor<CL>([&](auto Ci) HC_INL {
@@ -322,6 +353,11 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       HC_TRACE();
       if (stage_acc) sync();  // stash (acc) reads done before the next residue stashes F
     }
+  }
+  if constexpr (TMST) {
+    tmem_fence_before();
+    __syncthreads();
+    if (threadIdx.x < 32) tmem_dealloc(tm_base, TLc::COLS);
   }
 #undef HC_TRACE
 }
