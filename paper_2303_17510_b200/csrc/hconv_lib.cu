@@ -404,6 +404,9 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   static const bool same = std::getenv("HCONV_DEBUG_SAME_LINE") && std::getenv("HCONV_DEBUG_SAME_LINE")[0] == '1';
   if (same) a.lin.d_out = 0;
   a.ax.tabn = cl.tabn;
+  // the single-buffer Hermitian kernel keeps its accumulator in TMEM when its CTA owns the SM
+  static const bool no_tmacc = std::getenv("HCONV_NO_TMACC") && std::getenv("HCONV_NO_TMACC")[0] == '1';
+  a.tm_acc = (!no_tmacc && cl.stage != 3 && ap.dev.sym == hc::SYM_HERMITIAN && cl.smem > 116 * 1024) ? 1 : 0;
   // HCONV_TRACE=1: phase timestamps (clock64) of CTA 0, printed to stderr (diagnostics)
   static const bool trace = std::getenv("HCONV_TRACE") && std::getenv("HCONV_TRACE")[0] == '1';
   unsigned long long* tbuf = nullptr;

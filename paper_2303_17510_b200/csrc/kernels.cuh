@@ -29,6 +29,8 @@ struct ConvArgs {
   unsigned long long* trace;  // optional phase timestamps of CTA 0 / thread 0 (HCONV_TRACE)
   int dbg;                    // diagnostics (HCONV_DBG bits, ping-pong kernel): 1 skip stores,
                               // 2 skip pass-0 loads, 4 skip the product, 8 skip the inverse
+  int tm_acc = 0;             // k_conv1d, Hermitian: the CTA owns the SM, so the residue
+                              // accumulator may live in tensor memory (512 columns)
 };
 
 struct FwdArgs {
@@ -186,6 +188,59 @@ __device__ __forceinline__ void stage_tables(double2* tb, const AxisDev& a, int 
 // accumulator are brought on chip by TMA bulk copies issued one phase ahead -- the next line
 // copy starts as soon as the previous transform has released the exchange buffer, so the
 // HBM/L2 latency overlaps the butterflies of the current transform.
+// Hermitian post-processing with the residue accumulator in tensor memory: the same quads as
+// herm_store_quads (block_io.cuh), iterated a fixed NIT times per thread so that the
+// warp-collective tcgen05 loads / stores stay convergent; each iteration's four outputs keep
+// their four accumulator values in the thread's own TMEM columns (16 per iteration).  FIRST: no
+// accumulator yet; FINAL: add, scale and write the outputs instead of storing back.
+template <int NIT, int NS1>
+__device__ __forceinline__ void herm_quads_tm(const AxisDev& a, const double2* tb, double2* out, long long es,
+                                              double scale, const double2* Z, int v, int tid, int T, uint32_t ta,
+                                              bool first, bool final_) {
+  const int Bc = a.Bc, B = a.B, S = a.S, half = Bc / 2;
+  const double2 one = make_double2(1.0, 0.0);
+  const double2 zBc = v ? tH(a, tb, v) : one;
+  const double2 zB = v ? tC(a, tb, v, 1) : one;
+#pragma unroll 1
+  for (int it = 0; it < NIT; ++it) {
+    const int k0 = tid + it * T;
+    const bool kv = k0 <= half;
+    const int k = kv ? k0 : 0;
+    const int j[4] = {k, B - k, Bc - k, Bc + k};
+    const bool ok[4] = {kv && k < S, kv && k > 0 && B - k < S, kv && Bc - k != k && Bc - k < S,
+                        kv && k > 0 && k != half && Bc + k < S};
+    const double2 zk = Z[k];
+    const double2 zm = cconj(Z[k == 0 ? 0 : Bc - k]);
+    const double2 e = cscale(cadd(zk, zm), 0.5);
+    const double2 d = cscale(csub(zk, zm), 0.5);
+    const double2 o = make_double2(d.y, -d.x);
+    const double2 tB = cmul(tBh(a, tb, k / NS1), tBl(a, tb, k % NS1));
+    const double2 wk = cadd(e, cmulc(o, tB));
+    const double2 wm = csub(cconj(e), cmul(tB, cconj(o)));
+    double2 w[4] = {wk, cconj(wk), wm, cconj(wm)};
+    if (v) {
+      const double2 zvk = cmul(tZ(a, tb, v, k % NS1), tU(a, tb, v, k / NS1));
+      w[0] = cmulc(w[0], zvk);
+      w[1] = cmulc(cmul(w[1], zvk), zB);
+      w[2] = cmulc(cmul(w[2], zvk), zBc);
+      w[3] = cmulc(cmulc(w[3], zvk), zBc);
+    }
+    if (!first) {
+      double2 acc[4];
+      tm_ld4(ta + 16 * it, acc);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = cadd(w[u], acc[u]);
+    }
+    if (!final_) {
+      tm_st4(ta + 16 * it, w);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (ok[u]) __stcs(out + (long long)j[u] * es, cscale(w[u], scale));
+    }
+  }
+}
+
 // HC_CONV_TMEM=1: the register stash of the first spectrum (STASH_REGS) lives in tensor memory
 // instead (frees Cfg::ES complex registers per thread; 128 columns per CTA at most)
 #ifndef HC_CONV_TMEM
@@ -198,6 +253,11 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
   __shared__ uint32_t tm_base;
   using TLc = TmemLayout<Cfg::T * G, Cfg::ES, 0>;
   constexpr bool TMST = HC_CONV_TMEM && STASH_REGS && TLc::FITS && TLc::COLS <= 128;
+  // Hermitian accumulator in TMEM (host sets p.tm_acc when the CTA owns the SM)
+  constexpr int NIT = (Cfg::N / 2) / Cfg::T + 1;
+  using TLa = TmemLayout<Cfg::T * G, Cfg::ES, 4 * NIT>;
+  constexpr bool TMACC = TMST && SYM == SYM_HERMITIAN && TLa::FITS && G == 1;
+  const bool tm_acc = TMACC && p.tm_acc;
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
   const int g = threadIdx.x / T, tid = threadIdx.x % T;
   double2* tb = smem;
@@ -219,13 +279,14 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
     fence_mbar_init();
   }
   if constexpr (TMST) {
-    if (threadIdx.x < 32) tmem_alloc(&tm_base, TLc::COLS);
+    if (threadIdx.x < 32) tmem_alloc(&tm_base, tm_acc ? TLa::COLS : TLc::COLS);
     tmem_fence_before();
     __syncthreads();
     tmem_fence_after();
   }
   sync();
-  const uint32_t tf = TMST ? TLc::f_addr(tm_base) : 0u;
+  const uint32_t tf = TMST ? (tm_acc ? TLa::f_addr(tm_base) : TLc::f_addr(tm_base)) : 0u;
+  const uint32_t ta = tm_acc ? TLa::a_addr(tm_base) : 0u;
   uint32_t ph_in = 0, ph_acc = 0;
   const uint32_t row_bytes = (uint32_t)a.S * 16u;
   const long long es = p.lin.es, step = (long long)gridDim.x * G;
@@ -334,7 +395,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       });
       HC_TRACE();
       const double2* acc = nullptr;
-      if (res > 0) {
+      if (res > 0 && !tm_acc) {
         if (stage_acc) {
           mbar_wait(bar_acc, ph_acc);
           ph_acc ^= 1;
@@ -345,7 +406,19 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       }
       const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
       if constexpr (SYM == SYM_HERMITIAN) {
-        store_herm<Cfg>(v, a, tp, em, res, tid, X, sync);
+        if (tm_acc) {
+          constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1);
+          sfor<C0>([&](auto Ci) HC_INL {
+            constexpr int c = Ci;
+            const int b = tid + c * Cfg::T;
+            if (bvalid<Cfg, 0>(c, tid)) sfor<R0>([&](auto Ai) HC_INL { X[Ns1 * Ai + b] = v[c * R0 + Ai]; });
+          });
+          sync();
+          herm_quads_tm<NIT, Ns1>(a, tp, p.out + base, es, 1.0 / (double)a.qm, X, res, tid, Cfg::T, ta, res == 0, last);
+          sync();
+        } else {
+          store_herm<Cfg>(v, a, tp, em, res, tid, X, sync);
+        }
         if (stage == 1 && tid == 0 && fnext) tma_copy(IN, fnext, row_bytes, bar_in);
       } else {
         store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
@@ -355,9 +428,10 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
     }
   }
   if constexpr (TMST) {
+    tmem_wait_st();
     tmem_fence_before();
     __syncthreads();
-    if (threadIdx.x < 32) tmem_dealloc(tm_base, TLc::COLS);
+    if (threadIdx.x < 32) tmem_dealloc(tm_base, tm_acc ? TLa::COLS : TLc::COLS);
   }
 #undef HC_TRACE
 }
