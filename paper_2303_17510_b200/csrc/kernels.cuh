@@ -130,9 +130,10 @@ __device__ __forceinline__ void store_herm(const double2 (&v)[Cfg::E], const Axi
 //   W_s = (f_s + conj f_{B-s} [zeta^{-vB}]) zeta^{vs},  e = W_k + conj W_{Bc-k},
 //   o = (W_k - conj W_{Bc-k}) zeta_B^k,  Z'_k = e + i o,  Z'_{Bc-k} = conj e + i conj o.
 // The caller synchronises before reading Z' in pass-0 layout (load_plain).
-template <int NT>
+template <int NT, int NS1>
 __device__ __forceinline__ void herm_pack(double2* X, const AxisDev& a, const double2* tb, int v, int tid) {
-  const int Bc = a.Bc, B = a.B, S = a.S, half = Bc / 2, ns1 = a.ns1;
+  const int Bc = a.Bc, B = a.B, S = a.S, half = Bc / 2;
+  constexpr int ns1 = NS1;  // == a.ns1 (Bc / R0): compile-time, so k / ns1 is a shift or a multiply
   const double2 one = make_double2(1.0, 0.0);
   const double2 cH = v ? tb[a.oH + v] : one;            // zeta_qm^{v Bc}
   const double2 c1 = v ? tb[a.oC + v * a.nc + 1] : one;  // zeta_qm^{v B}
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
           ph_in ^= 1;
           HC_TRACE();
           if constexpr (SYM == SYM_HERMITIAN) {
-            herm_pack<T>(IN, a, tp, res, tid);
+            herm_pack<T, Cfg::Ns(1)>(IN, a, tp, res, tid);
             sync();
             load_plain<Cfg>(v, IN, tid);
           } else {
@@ -708,7 +709,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) {
-          herm_pack<T>(X, a, tb, res, tid);
+          herm_pack<T, Cfg::Ns(1)>(X, a, tb, res, tid);
           sync();
           load_plain<Cfg>(v, X, tid);
         } else {
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) {
-          herm_pack<T>(Y, a, tb, res, tid);
+          herm_pack<T, Cfg::Ns(1)>(Y, a, tb, res, tid);
           sync();
           load_plain<Cfg>(v, Y, tid);
         } else {
