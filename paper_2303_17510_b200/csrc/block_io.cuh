@@ -260,6 +260,22 @@ __device__ __forceinline__ void herm_store_quads(const AxisDev& a, const double2
   const double2 one = make_double2(1.0, 0.0);
   const double2 zBc = v ? tH(a, tb, v) : one;     // zeta_qm^{v Bc}
   const double2 zB = v ? tC(a, tb, v, 1) : one;   // zeta_qm^{v B}
+  if (S <= half) {
+    // heavily padded lines: every stored output is a quad's first element w_k (the other three
+    // lie beyond the data), so only w_k is formed
+    for (int k = tid; k < S; k += T) {
+      const double2 accv = em.acc ? em.acc[k * em.aes] : make_double2(0.0, 0.0);
+      const double2 zk = Z[k];
+      const double2 zm = cconj(Z[k == 0 ? 0 : Bc - k]);
+      const double2 e = cscale(cadd(zk, zm), 0.5);
+      const double2 d = cscale(csub(zk, zm), 0.5);
+      const double2 o = make_double2(d.y, -d.x);
+      double2 wk = cadd(e, cmulc(o, cmul(tBh(a, tb, k / NS1), tBl(a, tb, k % NS1))));
+      if (v) wk = cmulc(wk, cmul(tZ(a, tb, v, k % NS1), tU(a, tb, v, k / NS1)));
+      em.put(k, wk, accv);
+    }
+    return;
+  }
   for (int k = tid; k <= half; k += T) {
     int j[4] = {k, B - k, Bc - k, Bc + k};
     bool ok[4] = {k < S, k > 0 && B - k < S, Bc - k != k && Bc - k < S, k > 0 && k != half && Bc + k < S};

@@ -141,6 +141,20 @@ __device__ __forceinline__ void herm_pack(double2* X, const AxisDev& a, const do
   const double2* Ur = tb + (a.oU + v * a.nu);
   const double2* Bl = tb + a.oBl;
   const double2* Bh = tb + a.oBh;
+  if (S <= half) {
+    // heavily padded lines (S <= Bc/2, e.g. c5's z-lines, 256 of 1024): only x1 = f_k is
+    // nonzero in a quad (Bc - k, B - k and Bc + k all lie beyond the data), so W_{Bc-k} = 0,
+    // e = W_k and o = W_k zeta_B^k; quads with k >= S write zeros
+    for (int k = tid; k <= half; k += NT) {
+      const int kh = k / ns1, kl = k - kh * ns1;
+      double2 wk = k < S ? X[k] : make_double2(0.0, 0.0);
+      if (v) wk = cmul(wk, cmul(Zr[kl], Ur[kh]));  // zeta_qm^{v k}
+      const double2 o = cmul(wk, cmul(Bh[kh], Bl[kl]));
+      X[k] = make_double2(wk.x - o.y, wk.y + o.x);
+      if (k != 0 && k != half) X[Bc - k] = make_double2(wk.x + o.y, o.x - wk.y);
+    }
+    return;
+  }
   for (int k = tid; k <= half; k += NT) {
     const int kh = k / ns1, kl = k - kh * ns1;
     const int s2 = Bc - k;
