@@ -633,6 +633,11 @@ __device__ __forceinline__ void acc_tmem_pp(double2 (&v)[Cfg::E], const AxisDev&
 #ifndef HC_PP_TMEM_F
 #define HC_PP_TMEM_F 1
 #endif
+// HC_PP_TMEM_SHARED=1: TMEM stash / accumulator also for kernels with several CTAs per SM when
+// their columns fit together (measured slower for c1's 2048-point plan, 0.039 -> 0.044 ms: off)
+#ifndef HC_PP_TMEM_SHARED
+#define HC_PP_TMEM_SHARED 0
+#endif
 // HC_PP_DIRECT=1: with the accumulator in TMEM, the last residue writes its outputs straight from
 // registers (streaming stores) instead of assembling them in Y for a bulk store, and Y takes the
 // next line's g as soon as the inverse releases it (measured slower on B200: c2 0.795 -> 0.825 ms,
@@ -654,7 +659,11 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
   // tensor memory for the stashed spectrum F and the residue accumulator: kernels whose two
   // line buffers exclude a second CTA on the SM (so the whole TMEM is this CTA's)
   // (F in TMEM too frees X right after the f transform: c2 0.795 ms vs 0.815 with F in X)
-  constexpr bool TM_OK = !STASH_REGS && 2 * Cfg::XS * G * 16 > 116 * 1024;
+  // ... or whose TMEM columns fit next to every other CTA shared memory admits on the SM
+  using TLmax = TmemLayout<T * G, Cfg::ES, Cfg::C(0) * Cfg::R(0)>;
+  constexpr int kCtasPerSm = (232448 / 16) / (2 * Cfg::XS * G + Cfg::MT);
+  constexpr bool TM_OK = !STASH_REGS && TLmax::FITS &&
+                         (2 * Cfg::XS * G * 16 > 116 * 1024 || (HC_PP_TMEM_SHARED && TLmax::COLS * kCtasPerSm <= 512));
   constexpr bool TM_F = HC_PP_TMEM_F && TM_OK;
   using TL = TmemLayout<T * G, TM_F ? Cfg::ES : 0, Cfg::C(0) * Cfg::R(0)>;
   constexpr bool TMS = HC_PP_TMEM && TM_OK && TL::FITS;
