@@ -27,7 +27,8 @@
  *   hconv_plan_create        SPEC.md:400-403 Conv1dPlan, SPEC.md:469-472 ConvPlanND,
  *                            SPEC.md:533-550 tune_1d/tune_nd (when an axis has m == 0)
  *   hconv_convolve           SPEC.md:406-423 convolve/convolveC/convolveH,
- *                            SPEC.md:475-483 convolve_nd
+ *                            SPEC.md:475-483 convolve_nd (+ x-slabs over G ranks, hconv_slab)
+ *   hconv_plan_slab          (no reference counterpart: the slab extent of a rank)
  * Exceptions of the reference (std::invalid_argument, plan.cpp:36-38,67,77-80,92-93)
  * become HCONV_INVALID_ARG; the message is available from hconv_last_error().
  */
@@ -137,17 +138,49 @@ typedef struct hconv_desc {
   size_t A, B;           /* inputs / outputs of the multiplication operator */
   int mult;              /* hconv_mult */
   size_t C;              /* number of independent copies (1D lines or N-D arrays); 0 = 1 */
-  size_t dist;           /* elements between copies; 0 = stored length (N-D: array size) */
+  size_t dist;           /* 1D: elements between copies, >= the data length; 0 = the data length
+                          * (L, or ceil(L/2) for Hermitian -- K-length storage, SURVEY 8(a) note;
+                          * not hconv_stored_length).  N-D: must be 0 (contiguous arrays). */
   int device;            /* CUDA ordinal (ignored by the oracle) */
   int flags;             /* reserved, 0 */
   hconv_mult_fn mult_fn; /* HCONV_MULT_CALLBACK: the operator (else ignored) */
   void* mult_user;       /* passed through to mult_fn */
+  const struct hconv_slab* slab; /* NULL: one device holds the whole problem; else x-slab decomposition
+                           * (dims 2 or 3, C == 1; the struct is copied at plan creation) */
 } hconv_desc;
+
+/* ---- multi-GPU slab decomposition (2D / 3D, north star item 3) ----
+ * The reference has no distributed code (SPEC.md:512 lists MPI decomposition as a non-goal);
+ * this extends ConvPlanND / convolve_nd to x-slabs over G ranks.  With
+ * hconv_desc.slab != NULL the arrays passed to hconv_convolve are this rank's x-slab
+ * [nx][Ly] (2D) or [nx][Ly][Lz] (3D) of the global arrays, nx and the first row x0 given by
+ * hconv_plan_slab().  The outer padded FFT runs along the locally complete axis y; per y residue
+ * the spectral y-lines are transposed (all-to-all) so that every rank holds nk complete x-lines,
+ * the (d-1)-D subconvolutions run locally, and a second all-to-all brings them back before the
+ * inverse y-FFT.  Every m must be given (tune on one rank and broadcast the choice).
+ * Exchange: an NCCL communicator (CUDA library: ncclComm_t over NVLink / NVSwitch, grouped
+ * ncclSend / ncclRecv on a plan-owned stream, overlapped chunk by chunk with the
+ * subconvolutions), or, when nccl_comm is NULL, the caller's all-to-all callback.            */
+/* All-to-all-v over the ranks of the slab: send[sdispls[h] .. + scounts[h]) goes to rank h,
+ * recv[rdispls[h] .. + rcounts[h]) comes from rank h; counts and displacements in complex128
+ * elements.  CUDA library: device pointers, ordered on `stream`; oracle: host pointers.
+ * Return 0 on success (anything else aborts with HCONV_NCCL_ERROR).                         */
+typedef int (*hconv_exchange_fn)(const void* send, const size_t* scounts, const size_t* sdispls, void* recv,
+                                 const size_t* rcounts, const size_t* rdispls, void* user, void* stream);
+typedef struct hconv_slab {
+  int rank, nranks;           /* this rank, number of ranks G (1 <= G) */
+  void* nccl_comm;            /* ncclComm_t (CUDA library only), or NULL */
+  hconv_exchange_fn exchange; /* used when nccl_comm is NULL */
+  void* exchange_user;
+  size_t chunks;              /* k-line chunks per exchange (pipelining); 0 = library default */
+} hconv_slab;
 
 typedef struct hconv_plan hconv_plan;
 
 hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** plan);
 hconv_status hconv_plan_params(const hconv_plan* plan, int axis, hconv_params* out);
+/* Slab plans: first row x0 and row count nx of this rank's x-slab (nx may be 0). */
+hconv_status hconv_plan_slab(const hconv_plan* plan, size_t* x0, size_t* nx);
 /* Bytes of device scratch the plan owns (0 for the oracle). */
 size_t hconv_plan_workspace_bytes(const hconv_plan* plan);
 /* in[A], out[B]: complex128 arrays with the stored layout of the descriptor.

@@ -21,6 +21,13 @@ int hconv_plan_report(const hconv_plan* plan, double* out, int cap);
  *              F0 <- F0 F0, F1 <- F0 F1, F2 <- F1 F1 (complex, or real for Hermitian blocks)
  * Returns NULL for an unknown id. */
 hconv_mult_fn hconv_example_mult(int which);
+/* NCCL bootstrap for slab plans (hconv_slab.nccl_comm).  The library binds NCCL at run time
+ * (the libnccl.so.2 already loaded by the process, e.g. torch's, else the system one).
+ * hconv_nccl_unique_id writes the 128-byte ncclUniqueId on one rank; every rank passes the same
+ * bytes to hconv_nccl_comm_init (device = its CUDA ordinal).  HCONV_NCCL_ERROR on failure.   */
+hconv_status hconv_nccl_unique_id(void* id128);
+hconv_status hconv_nccl_comm_init(const void* id128, int nranks, int rank, int device, void** comm);
+hconv_status hconv_nccl_comm_destroy(void* comm);
 /* Radix plan of the kernel serving an axis ("16x16x24", "direct", ...). */
 const char* hconv_plan_kernel(const hconv_plan* plan, int axis);
 #ifdef __cplusplus

@@ -31,12 +31,14 @@
 // compiled into oracle/_ref/ (oracle/Makefile); the arithmetic is checked against the
 // SPEC known-answer examples (tests/golden/spec_kats.json) and naive padded DFTs.
 #include "../include/hconv.h"
+#include "../paper_2303_17510_b200/csrc/slab.hpp"
 
 #include <omp.h>
 
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <memory>
 #include <cstdint>
 #include <cstring>
 #include <stdexcept>
@@ -903,10 +905,130 @@ hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, co
   });
 }
 
+struct OracleSlab;
+struct OracleSlabDel {
+  void operator()(OracleSlab* s) const;
+};
 struct hconv_plan {
   hconv_desc d;
   std::vector<AxisP> ax;
+  std::unique_ptr<OracleSlab, OracleSlabDel> slab;
 };
+
+// ---- x-slab decomposition (hconv_desc.slab): the product's driver (slab.hpp) over host buffers
+// and the oracle's padded FFTs, so the CPU tests (gloo, several processes) check the product's
+// index arithmetic and schedule against the oracle's own single-process convolve_nd.  The
+// reference has no distributed code; nothing here restates it.
+struct OracleSlabOps {
+  OracleSlab* st = nullptr;
+  void* alloc(size_t elems) { return new cd[elems](); }
+  void free(void* p) { delete[] (cd*)p; }
+  void fwd(size_t r, const void* f, void* F);
+  void bwd(size_t r, const void* W, void* h, bool acc, double scale);
+  void inner(size_t count, void* const* T);
+  void copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows, bool) {
+    for (size_t i = 0; i < rows; ++i) std::copy((const cd*)src + i * spitch, (const cd*)src + i * spitch + width, (cd*)dst + i * dpitch);
+  }
+  void exchange(const void* send, const size_t* sc, const size_t* sd, void* recv, const size_t* rc, const size_t* rd);
+  void comm_after_compute() {}
+  void mark_comm(size_t) {}
+  void compute_after_comm(size_t) {}
+};
+struct OracleSlab {
+  hconv_slab cfg{};
+  hslab::Geometry g;
+  hconv_params py{};
+  hconv_plan* inner = nullptr;
+  OracleSlabOps ops;
+  std::unique_ptr<hslab::Driver<OracleSlabOps>> drv;
+  ~OracleSlab();
+};
+static void slab_check(hconv_status st, const char* what) {
+  if (st != HCONV_OK) throw std::invalid_argument(std::string(what) + ": " + g_err);
+}
+void OracleSlabOps::fwd(size_t r, const void* f, void* F) {
+  const hslab::Geometry& g = st->g;
+  const size_t nxz = g.nx() * g.Z;
+  const hconv_lines lin{nxz, g.Z, g.Ly * g.Z, 1, g.Z}, lspec{nxz, nxz, 0, 1, nxz};
+  if (nxz) slab_check(hconv_pfft_forward_lines(&st->py, f, &lin, r, F, &lspec, nullptr), "slab forward");
+}
+void OracleSlabOps::bwd(size_t r, const void* W, void* h, bool acc, double scale) {
+  const hslab::Geometry& g = st->g;
+  const size_t nxz = g.nx() * g.Z;
+  const hconv_lines lin{nxz, g.Z, g.Ly * g.Z, 1, g.Z}, lspec{nxz, nxz, 0, 1, nxz};
+  if (nxz) slab_check(hconv_pfft_backward_lines(&st->py, W, &lspec, r, h, &lin, acc ? 1 : 0, scale, nullptr), "slab backward");
+}
+void OracleSlabOps::inner(size_t count, void* const* T) {
+  hconv_plan* P = st->inner;
+  const size_t keep = P->d.C;
+  P->d.C = count;
+  const hconv_status rc = hconv_convolve(P, (const void* const*)T, T, nullptr);
+  P->d.C = keep;
+  slab_check(rc, "slab subconvolution");
+}
+void OracleSlabOps::exchange(const void* send, const size_t* sc, const size_t* sd, void* recv, const size_t* rc,
+                             const size_t* rd) {
+  const hslab::Geometry& g = st->g;
+  if (!st->cfg.exchange) {  // one rank: the only segment is its own
+    std::copy((const cd*)send + sd[0], (const cd*)send + sd[0] + sc[0], (cd*)recv + rd[0]);
+    return;
+  }
+  (void)g;
+  const int r = st->cfg.exchange(send, sc, sd, recv, rc, rd, st->cfg.exchange_user, nullptr);
+  if (r != 0) throw std::runtime_error("slab exchange callback returned " + std::to_string(r));
+}
+OracleSlab::~OracleSlab() {
+  drv.reset();
+  if (inner) hconv_plan_destroy(inner);
+}
+void OracleSlabDel::operator()(OracleSlab* s) const { delete s; }
+
+static void build_slab(hconv_plan* p) {
+  const hconv_desc* desc = &p->d;
+  const hconv_slab& cfg = *desc->slab;
+  const int d = desc->dims;
+  if (d < 2) throw std::invalid_argument("slab decomposition is for 2D and 3D convolutions");
+  if (d == 2 && p->ax[1].P.sym == HCONV_HERMITIAN) throw std::invalid_argument("2D Hermitian slabs are not supported");
+  if (desc->C > 1) throw std::invalid_argument("slab plans convolve one global array (C must be 0 or 1)");
+  if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks) throw std::invalid_argument("slab: bad rank / nranks");
+  if (cfg.nranks > 1 && !cfg.exchange) throw std::invalid_argument("the oracle exchanges through the callback only");
+  for (int k = 0; k < d; ++k)
+    if (desc->axis[k].m == 0) throw std::invalid_argument("slab plans need every m (tune on one rank, broadcast)");
+  auto st = std::unique_ptr<OracleSlab, OracleSlabDel>(new OracleSlab());
+  st->cfg = cfg;
+  to_abi(p->ax[1].P, &st->py);
+  const Params& Py = p->ax[1].P;
+  st->g = hslab::make_geometry(cfg.rank, cfg.nranks, p->ax[0].stored, p->ax[1].stored, d == 3 ? p->ax[2].stored : 1,
+                               block_len(Py), Py.n, 1.0 / (double)(Py.q * Py.m), cfg.chunks);
+  hconv_desc in{};
+  in.dims = d - 1;
+  in.axis[0] = desc->axis[0];
+  in.axis[0].symmetry = p->ax[0].P.sym;
+  if (d == 3) {
+    in.axis[1] = desc->axis[2];
+    in.axis[1].symmetry = p->ax[2].P.sym;
+  }
+  in.A = desc->A;
+  in.B = desc->B;
+  in.mult = desc->mult;
+  in.C = std::max<size_t>(1, st->g.max_chunk());
+  in.mult_fn = desc->mult_fn;
+  in.mult_user = desc->mult_user;
+  slab_check(hconv_plan_create(&in, &st->inner), "slab inner plan");
+  st->ops.st = st.get();
+  st->drv = std::make_unique<hslab::Driver<OracleSlabOps>>(st->g, desc->A, desc->B, st->ops);
+  p->slab = std::move(st);
+  p->d.slab = nullptr;
+}
+static void slab_convolve(hconv_plan* p, const void* const* in, void* const* out) {
+  OracleSlab& S = *p->slab;
+  const size_t n = S.g.nx() * S.g.Ly * S.g.Z;
+  std::vector<std::vector<cd>> acc(p->d.B, std::vector<cd>(std::max<size_t>(1, n)));
+  std::vector<void*> ap(p->d.B);
+  for (size_t b = 0; b < p->d.B; ++b) ap[b] = acc[b].data();
+  S.drv->run(in, ap.data());
+  for (size_t b = 0; b < p->d.B; ++b) std::copy(acc[b].begin(), acc[b].begin() + n, (cd*)out[b]);
+}
 
 hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
   return guarded([&] {
@@ -933,6 +1055,18 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
       ap.stored = stored_len(ap.P);
       p->ax.push_back(ap);
     }
+    if (desc->dims == 1 && desc->dist != 0 && desc->dist < p->ax[0].stored) {
+      delete p;
+      throw std::invalid_argument("dist smaller than the data length: copies would overlap");
+    }
+    if (desc->slab) {
+      try {
+        build_slab(p);
+      } catch (...) {
+        delete p;
+        throw;
+      }
+    }
     *out = p;
   });
 }
@@ -942,6 +1076,14 @@ hconv_status hconv_plan_params(const hconv_plan* p, int axis, hconv_params* o) {
   return HCONV_OK;
 }
 size_t hconv_plan_workspace_bytes(const hconv_plan*) { return 0; }
+hconv_status hconv_plan_slab(const hconv_plan* p, size_t* x0, size_t* nx) {
+  return guarded([&] {
+    if (!p || !x0 || !nx) throw std::invalid_argument("null argument");
+    if (!p->slab) throw std::invalid_argument("not a slab plan");
+    *x0 = p->slab->g.xs[p->slab->g.rank].lo;
+    *nx = p->slab->g.nx();
+  });
+}
 hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* out, void* /*stream*/) {
   return guarded([&] {
     if (!p || !in || !out) throw std::invalid_argument("null argument");
@@ -952,7 +1094,9 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
     for (size_t b = 0; b < Bo; ++b) if (!out[b]) throw std::invalid_argument("null output array");
     // a user callback is not assumed thread-safe: the oracle calls it from one thread
     const bool par = mu.kind == HCONV_MULT_PRODUCT;
-    if (p->d.dims == 1) {
+    if (p->slab) {
+      slab_convolve(p, in, out);
+    } else if (p->d.dims == 1) {
       const size_t Ls = p->ax[0].stored, dist = p->d.dist ? p->d.dist : Ls, C = p->d.C ? p->d.C : 1;
       std::vector<std::vector<cd>> res(Bo, std::vector<cd>(C * Ls));
       std::string err;

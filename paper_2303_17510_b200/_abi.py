@@ -21,6 +21,24 @@ MultFn = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_void_p), C.c_size_t, C.c_size_t, C.c
                      C.c_void_p)
 
 
+# include/hconv.h hconv_exchange_fn: (send, scounts, sdispls, recv, rcounts, rdispls, user, stream) -> int
+ExchangeFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.c_void_p,
+                         C.POINTER(C.c_size_t), C.POINTER(C.c_size_t), C.c_void_p, C.c_void_p)
+
+
+class Slab(C.Structure):
+    """hconv_slab: x-slab decomposition over `nranks` ranks (NCCL communicator or callback)."""
+
+    _fields_ = [
+        ("rank", C.c_int),
+        ("nranks", C.c_int),
+        ("nccl_comm", C.c_void_p),
+        ("exchange", C.c_void_p),
+        ("exchange_user", C.c_void_p),
+        ("chunks", C.c_size_t),
+    ]
+
+
 class Params(C.Structure):
     """hconv_params == proj/include/hconv/plan.hpp:39-62 PlanParams."""
 
@@ -48,6 +66,7 @@ class Desc(C.Structure):
         ("flags", C.c_int),
         ("mult_fn", C.c_void_p),
         ("mult_user", C.c_void_p),
+        ("slab", C.c_void_p),
     ]
 
 
@@ -87,6 +106,7 @@ PROTOTYPES = {
     ),
     "hconv_plan_create": (C.c_int, [C.POINTER(Desc), C.POINTER(C.c_void_p)]),
     "hconv_plan_params": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(Params)]),
+    "hconv_plan_slab": (C.c_int, [C.c_void_p, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
     "hconv_plan_workspace_bytes": (C.c_size_t, [C.c_void_p]),
     "hconv_convolve": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_void_p]),
     "hconv_convolve_host": (C.c_int, [C.c_void_p, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
@@ -101,6 +121,9 @@ EXT_PROTOTYPES = {
     "hconv_plan_report": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_int]),
     "hconv_plan_kernel": (C.c_char_p, [C.c_void_p, C.c_int]),
     "hconv_example_mult": (C.c_void_p, [C.c_int]),
+    "hconv_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "hconv_nccl_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "hconv_nccl_comm_destroy": (C.c_int, [C.c_void_p]),
 }
 
 

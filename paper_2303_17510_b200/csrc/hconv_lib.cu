@@ -7,6 +7,8 @@
 //   ConvPlanND
 //   tune_1d / tune_nd    SPEC.md:518-572, PAPER.md:894-914 (device events replace the CPU clock)
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the functions are bound at run time (nccl() below)
 
 #include <algorithm>
 #include <cmath>
@@ -25,6 +27,7 @@
 #include "../../include/hconv_ext.h"
 #include "plan.hpp"
 #include "registry.cuh"
+#include "slab.hpp"
 
 namespace hc {
 void registry_sym0(KernelEntry* out, int* count);
@@ -44,6 +47,9 @@ struct CudaError : std::runtime_error {
 struct Unsupported : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 #define CK(x)                                                                                 \
   do {                                                                                        \
@@ -51,12 +57,61 @@ struct Unsupported : std::runtime_error {
     if (e_ != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Diagnostics switches, read once from the environment (HCONV_*; tools/README.md).  None of
+// them is needed in production: the defaults are the measured-best choices.
+struct Diag {
+  bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, sync_mult;
+  int dbg;
+  double general_block_mb, nd_block_mb;
+  long long host_chunks;
+  Diag() {
+    auto on = [](const char* n) { const char* v = std::getenv(n); return v && v[0] == '1'; };
+    auto num = [](const char* n, double d) { const char* v = std::getenv(n); return v ? std::atof(v) : d; };
+    poison = on("HCONV_POISON");
+    no_stage = on("HCONV_NO_STAGE");
+    no_pp = on("HCONV_NO_PP");
+    pp2 = !(std::getenv("HCONV_PP2") && std::getenv("HCONV_PP2")[0] == '0');
+    same_line = on("HCONV_DEBUG_SAME_LINE");
+    no_tmacc = on("HCONV_NO_TMACC");
+    trace = on("HCONV_TRACE");
+    no_cols = on("HCONV_NO_COLS");
+    no_cols_pp = on("HCONV_NO_COLS_PP");
+    sync_mult = on("HCONV_SYNC_MULT");
+    dbg = (int)num("HCONV_DBG", 0);
+    general_block_mb = num("HCONV_GENERAL_BLOCK_MB", 256.0);
+    nd_block_mb = num("HCONV_ND_BLOCK_MB", 0.0);
+    host_chunks = (long long)num("HCONV_HOST_CHUNKS", 8);
+  }
+};
+const Diag& diag() {
+  static const Diag d;
+  return d;
+}
+
 // HCONV_POISON=1 (diagnostics): fill every scratch / work allocation with NaN so that a read
 // before write shows up in the results instead of reading zeros from fresh pages
 void poison(void* p, size_t bytes) {
-  static const bool on = std::getenv("HCONV_POISON") && std::getenv("HCONV_POISON")[0] == '1';
-  if (on) CK(cudaMemset(p, 0xff, bytes));
+  if (diag().poison) CK(cudaMemset(p, 0xff, bytes));
 }
+
+// Sets the plan's device for the duration of an ABI call and restores the caller's current
+// device on every exit path (the library must not change e.g. torch's current device).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int d) {
+    int cur = 0;
+    CK(cudaGetDevice(&cur));
+    if (cur != d) {
+      CK(cudaSetDevice(d));
+      prev = cur;
+    }
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+  DeviceGuard(const DeviceGuard&) = delete;
+  DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
 
 template <class F>
 hconv_status guarded(F&& f) {
@@ -71,6 +126,9 @@ hconv_status guarded(F&& f) {
   } catch (const CudaError& e) {
     g_err = e.what();
     return HCONV_CUDA_ERROR;
+  } catch (const NcclError& e) {
+    g_err = e.what();
+    return HCONV_NCCL_ERROR;
   } catch (const std::bad_alloc& e) {
     g_err = "host allocation failed";
     return HCONV_ALLOC;
@@ -355,12 +413,12 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
     c.smem = smem_conv(ap);
     return c;
   }
-  static const bool off = std::getenv("HCONV_NO_STAGE") && std::getenv("HCONV_NO_STAGE")[0] == '1';
+  const bool off = diag().no_stage;
   const int S = ap.dev.S;
   c.gs = k->xs + k->stash;
-  static const bool no_pp = std::getenv("HCONV_NO_PP") && std::getenv("HCONV_NO_PP")[0] == '1';
+  const bool no_pp = diag().no_pp;
   // (the ping-pong kernel reads every table from shared memory: all of them must fit)
-  if (!off && !no_pp && !k->pair && lin.es == 1 && S <= k->xs &&
+  if (!off && !no_pp && lin.es == 1 && S <= k->xs &&
       (size_t)(ap.tab_full + (size_t)k->G * 2 * k->xs) * sizeof(double2) <= kSmemCap) {
     c.stage = 3;  // ping-pong: X (f, its exchanges, stashed F) and Y (g, its and the inverse's exchanges)
     c.gs = 2 * k->xs;
@@ -371,8 +429,6 @@ ConvLayout conv_layout(const AxisPlan& ap, const hc::Lines& lin) {
   if (!off && lin.es == 1) {
     if (S <= k->xs) {
       c.stage = 1;
-    } else if (k->pair) {
-      c.stage = 0;  // the paired kernel stages both lines into X and Y or none
     } else if ((size_t)(k->mt + (size_t)k->G * (c.gs + std::max(S, ap.dev.Bc))) * sizeof(double2) <= kSmemCap) {
       // (the Hermitian packing writes Z'_k, k < Bc, into the staged line in place)
       c.stage = 2;
@@ -391,24 +447,22 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   if (lin.count == 0) return;
   const ConvLayout cl = conv_layout(ap, lin);
   // the paired ping-pong kernel where it exists (complex, L <= B; registry) -- HCONV_PP2=0 disables it
-  static const bool pp2_on = !(std::getenv("HCONV_PP2") && std::getenv("HCONV_PP2")[0] == '0');
+  const bool pp2_on = diag().pp2;
   const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
   const void* fn = pp2 ? ap.k->convpp2_fn : cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
   const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
   scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
   hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr, 0};
-  static const int dbg = std::getenv("HCONV_DBG") ? std::atoi(std::getenv("HCONV_DBG")) : 0;
-  a.dbg = dbg;
+  a.dbg = diag().dbg;
   // HCONV_DEBUG_SAME_LINE=1: every line reads/writes line 0 (L2-resident timing of the kernel
   // body without HBM; diagnostics only, results are meaningless)
-  static const bool same = std::getenv("HCONV_DEBUG_SAME_LINE") && std::getenv("HCONV_DEBUG_SAME_LINE")[0] == '1';
-  if (same) a.lin.d_out = 0;
+  if (diag().same_line) a.lin.d_out = 0;
   a.ax.tabn = cl.tabn;
   // the single-buffer Hermitian kernel keeps its accumulator in TMEM when its CTA owns the SM
-  static const bool no_tmacc = std::getenv("HCONV_NO_TMACC") && std::getenv("HCONV_NO_TMACC")[0] == '1';
+  const bool no_tmacc = diag().no_tmacc;
   a.tm_acc = (!no_tmacc && cl.stage != 3 && ap.dev.sym == hc::SYM_HERMITIAN && cl.smem > 116 * 1024) ? 1 : 0;
   // HCONV_TRACE=1: phase timestamps (clock64) of CTA 0, printed to stderr (diagnostics)
-  static const bool trace = std::getenv("HCONV_TRACE") && std::getenv("HCONV_TRACE")[0] == '1';
+  const bool trace = diag().trace;
   unsigned long long* tbuf = nullptr;
   if (trace && !ap.k->naive) {
     CK(cudaMalloc(&tbuf, 256 * sizeof(unsigned long long)));
@@ -432,7 +486,7 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
 
 // Column-tile variants for strided outer-axis lines (complex / centered radix kernels).
 bool use_cols(const AxisPlan& ap, const hc::Lines& lin) {
-  static const bool off = std::getenv("HCONV_NO_COLS") && std::getenv("HCONV_NO_COLS")[0] == '1';
+  const bool off = diag().no_cols;
   return !off && !ap.k->naive && ap.k->fwdc && lin.es > 1;
 }
 int cols_tabn(const AxisPlan& ap) {
@@ -450,7 +504,7 @@ int grid_cols(const void* fn, const KernelEntry* k, size_t smem, long long items
 // Pipelined column tiles (k_pfft_*_cols_pp): two tile buffers of gc x max(xs, rows) values plus
 // at least the middle-pass tables must fit; returns the staged table prefix (0 = does not fit).
 int cols_pp_tabn(const AxisPlan& ap, int rows, size_t* smem) {
-  static const bool off = std::getenv("HCONV_NO_COLS_PP") && std::getenv("HCONV_NO_COLS_PP")[0] == '1';
+  const bool off = diag().no_cols_pp;
   // only at the unpipelined kernel's tile width: narrower tiles cost more in DRAM row efficiency
   // than the pipelining recovers (c4 outer 4096-point columns, 2 -> 1 column per tile: 0.54 -> 0.69 ms)
   if (off || !ap.k->fwdcp || ap.k->gcp != ap.k->gc) return 0;
@@ -770,8 +824,17 @@ struct HostPipe {
   }
 };
 
+namespace {
+struct SlabState;
+void destroy_slab(SlabState* s);
+struct SlabDel {
+  void operator()(SlabState* s) const { destroy_slab(s); }
+};
+}  // namespace
+
 struct hconv_plan {
   hconv_desc d{};
+  std::unique_ptr<SlabState, SlabDel> slab;  // x-slab decomposition over G ranks (slab.hpp)
   int device = 0;
   std::vector<AxisPlan> ax;
   Scratch scratch;                    // conv1d accumulator slots
@@ -863,7 +926,7 @@ void apply_mult(const hconv_plan* P, double2* const* F, long long count, bool re
   }
   void* ptrs[kMaxArity];
   for (size_t a = 0; a < P->W(); ++a) ptrs[a] = F[a];
-  static const bool dsync = std::getenv("HCONV_SYNC_MULT") && std::getenv("HCONV_SYNC_MULT")[0] == '1';
+  const bool dsync = diag().sync_mult;
   if (dsync) CK(cudaDeviceSynchronize());
   const int rc = P->d.mult_fn(ptrs, P->d.A, P->d.B, (size_t)count, real ? 1 : 0, P->d.mult_user, s);
   if (dsync) CK(cudaDeviceSynchronize());
@@ -882,7 +945,7 @@ void conv1d_general(hconv_plan* P, const AxisPlan& ap, long long C, long long di
   const long long Bl = ap.dev.B, S = (long long)ap.data, n = ap.dev.n;
   const bool real = ap.dev.sym == hc::SYM_HERMITIAN;
   // work blocks per pass: HCONV_GENERAL_BLOCK_MB (default 256 MB of blocks and accumulators)
-  static const double block_mb = std::getenv("HCONV_GENERAL_BLOCK_MB") ? std::atof(std::getenv("HCONV_GENERAL_BLOCK_MB")) : 256.0;
+  const double block_mb = diag().general_block_mb;
   const long long per_line = (long long)(W * Bl + (n > 1 ? Bo * dist : 0)) * (long long)sizeof(double2);
   const long long chunk = std::max<long long>(1, std::min<long long>(C, (long long)(block_mb * 1048576.0 / per_line)));
   const long long acc_elems = (chunk - 1) * dist + S;
@@ -960,6 +1023,247 @@ void nd_level(hconv_plan* P, int level, long long NB, const double2* const* in, 
   }
 }
 
+// ------------------------------------------------------------ NCCL binding ---
+// Bound at run time to the libnccl.so.2 the process already has (torch's), else the system one:
+// the library itself has no link-time NCCL dependency (single-GPU users never load it).
+struct Nccl {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  std::string why;
+};
+const Nccl& nccl() {
+  static const Nccl n = [] {
+    Nccl r;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      r.why = std::string("libnccl.so.2 not found: ") + (dlerror() ? dlerror() : "");
+      return r;
+    }
+    auto sym = [&](const char* name) { return dlsym(h, name); };
+    r.GetUniqueId = (decltype(r.GetUniqueId))sym("ncclGetUniqueId");
+    r.CommInitRank = (decltype(r.CommInitRank))sym("ncclCommInitRank");
+    r.CommDestroy = (decltype(r.CommDestroy))sym("ncclCommDestroy");
+    r.GroupStart = (decltype(r.GroupStart))sym("ncclGroupStart");
+    r.GroupEnd = (decltype(r.GroupEnd))sym("ncclGroupEnd");
+    r.Send = (decltype(r.Send))sym("ncclSend");
+    r.Recv = (decltype(r.Recv))sym("ncclRecv");
+    r.GetErrorString = (decltype(r.GetErrorString))sym("ncclGetErrorString");
+    if (!r.GetUniqueId || !r.CommInitRank || !r.CommDestroy || !r.GroupStart || !r.GroupEnd || !r.Send || !r.Recv)
+      r.why = "libnccl.so.2 lacks a required symbol";
+    return r;
+  }();
+  if (!n.why.empty()) throw NcclError(n.why);
+  return n;
+}
+#define NC(x)                                                                                       \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess)                                                                          \
+      throw NcclError(std::string(#x) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r_) : "error")); \
+  } while (0)
+
+// ------------------------------------------------------------ slab plans ----
+// hconv_desc.slab != NULL: the x-slab decomposition of slab.hpp with device buffers, the y-axis
+// padded FFT kernels (k-major spectral layout), an inner (d-1)-D plan of this library for the
+// subconvolutions of one chunk of k-lines, and the exchange on a plan-owned stream.
+struct CudaSlabOps {
+  SlabState* st = nullptr;
+  cudaStream_t s = nullptr;  // the caller's (compute) stream of the current hconv_convolve
+  void* alloc(size_t elems);
+  void free(void* p) {
+    if (p) cudaFree(p);
+  }
+  void fwd(size_t r, const void* f, void* F);
+  void bwd(size_t r, const void* W, void* h, bool acc, double scale);
+  void inner(size_t count, void* const* T);
+  void copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows, bool on_comm);
+  void exchange(const void* send, const size_t* sc, const size_t* sd, void* recv, const size_t* rc, const size_t* rd);
+  void comm_after_compute();
+  void mark_comm(size_t tag);
+  void compute_after_comm(size_t tag);
+};
+
+struct SlabState {
+  hconv_slab cfg{};
+  hslab::Geometry g;
+  AxisPlan ay;                     // the outer (y) axis
+  hconv_plan* inner = nullptr;     // (d-1)-D subconvolutions of max_chunk copies
+  cudaStream_t sc = nullptr;       // communication stream
+  std::vector<cudaEvent_t> ev;     // per chunk: forward exchange done (comm -> compute)
+  cudaEvent_t ev_c = nullptr, ev_m = nullptr;  // compute -> comm, comm -> compute (all)
+  CudaSlabOps ops;
+  std::unique_ptr<hslab::Driver<CudaSlabOps>> drv;
+  std::vector<double2*> acc;       // accumulators for outputs that alias inputs (lazily)
+  ~SlabState() {
+    drv.reset();
+    for (double2* a : acc)
+      if (a) cudaFree(a);
+    if (inner) hconv_plan_destroy(inner);
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (ev_c) cudaEventDestroy(ev_c);
+    if (ev_m) cudaEventDestroy(ev_m);
+    if (sc) cudaStreamDestroy(sc);
+  }
+};
+void destroy_slab(SlabState* s) { delete s; }
+
+void* CudaSlabOps::alloc(size_t elems) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, elems * sizeof(double2)));
+  poison(p, elems * sizeof(double2));
+  return p;
+}
+// y-lines (x, z) of the x-slab [nx][Ly][Z] <-> the same lines k-major F[k][x][z]
+void CudaSlabOps::fwd(size_t r, const void* f, void* F) {
+  const hslab::Geometry& g = st->g;
+  const long long nxz = (long long)(g.nx() * g.Z), Z = (long long)g.Z;
+  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, nxz, 0, 1, nxz};
+  launch_fwd(st->ay, lin, lspec, (const double2*)f, F, (int)r, 0, s);
+}
+void CudaSlabOps::bwd(size_t r, const void* W, void* h, bool acc, double scale) {
+  const hslab::Geometry& g = st->g;
+  const long long nxz = (long long)(g.nx() * g.Z), Z = (long long)g.Z;
+  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, nxz, 0, 1, nxz};
+  launch_bwd(st->ay, lspec, lin, W, (double2*)h, acc ? (const double2*)h : nullptr, scale, (int)r, 0, s);
+}
+void CudaSlabOps::inner(size_t count, void* const* T) {
+  hconv_plan* P = st->inner;
+  std::vector<const double2*> in(P->d.A);
+  std::vector<double2*> out(P->d.B);
+  for (size_t a = 0; a < P->d.A; ++a) in[a] = (const double2*)T[a];
+  for (size_t b = 0; b < P->d.B; ++b) out[b] = (double2*)T[b];
+  if (P->d.dims == 1) conv1d(P, P->ax[0], (long long)count, (long long)P->ax[0].data, in.data(), out.data(), s);
+  else nd_level(P, 0, (long long)count, in.data(), out.data(), s);
+}
+void CudaSlabOps::copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows,
+                         bool on_comm) {
+  if (!rows || !width) return;
+  CK(cudaMemcpy2DAsync(dst, dpitch * sizeof(double2), src, spitch * sizeof(double2), width * sizeof(double2), rows,
+                       cudaMemcpyDeviceToDevice, on_comm ? st->sc : s));
+}
+void CudaSlabOps::exchange(const void* send, const size_t* sc, const size_t* sd, void* recv, const size_t* rc,
+                           const size_t* rd) {
+  const hslab::Geometry& g = st->g;
+  const int me = g.rank;
+  auto sp = [&](size_t off) { return (const char*)send + off * sizeof(double2); };
+  auto rp = [&](size_t off) { return (char*)recv + off * sizeof(double2); };
+  if (st->cfg.nccl_comm || !st->cfg.exchange) {
+    // this rank's own segment is a device copy on the communication stream
+    if (sc[me]) CK(cudaMemcpyAsync(rp(rd[me]), sp(sd[me]), sc[me] * sizeof(double2), cudaMemcpyDeviceToDevice, st->sc));
+    if (!st->cfg.nccl_comm) return;  // one rank, no communicator: the copy was the exchange
+    const Nccl& n = nccl();
+    ncclComm_t comm = (ncclComm_t)st->cfg.nccl_comm;
+    NC(n.GroupStart());
+    for (int h = 0; h < g.G; ++h) {
+      if (h == me) continue;
+      if (sc[h]) NC(n.Send(sp(sd[h]), 2 * sc[h], ncclFloat64, h, comm, st->sc));
+      if (rc[h]) NC(n.Recv(rp(rd[h]), 2 * rc[h], ncclFloat64, h, comm, st->sc));
+    }
+    NC(n.GroupEnd());
+    return;
+  }
+  const int r = st->cfg.exchange(send, sc, sd, recv, rc, rd, st->cfg.exchange_user, st->sc);
+  if (r != 0) throw NcclError("slab exchange callback returned " + std::to_string(r));
+}
+void CudaSlabOps::comm_after_compute() {
+  CK(cudaEventRecord(st->ev_c, s));
+  CK(cudaStreamWaitEvent(st->sc, st->ev_c, 0));
+}
+void CudaSlabOps::mark_comm(size_t tag) { CK(cudaEventRecord(st->ev[tag], st->sc)); }
+void CudaSlabOps::compute_after_comm(size_t tag) {
+  if (tag == (size_t)-1) {
+    CK(cudaEventRecord(st->ev_m, st->sc));
+    CK(cudaStreamWaitEvent(s, st->ev_m, 0));
+  } else {
+    CK(cudaStreamWaitEvent(s, st->ev[tag], 0));
+  }
+}
+
+// Slab plan: axis plans for parameter reports, the y kernels, the inner plan, the buffers.
+void build_slab(hconv_plan* P, const std::vector<hb::Symmetry>& syms, const std::vector<size_t>& data) {
+  const hconv_desc* desc = &P->d;
+  const hconv_slab& cfg = *desc->slab;
+  const int d = desc->dims;
+  if (d < 2) throw std::invalid_argument("slab decomposition is for 2D and 3D convolutions");
+  if (d == 2 && syms[1] == hb::Symmetry::Hermitian)
+    throw Unsupported("2D Hermitian slabs need the outer axis sharded (three transposes)");
+  if (desc->C > 1) throw std::invalid_argument("slab plans convolve one global array (C must be 0 or 1)");
+  if (cfg.nranks < 1 || cfg.rank < 0 || cfg.rank >= cfg.nranks) throw std::invalid_argument("slab: bad rank / nranks");
+  if (cfg.nranks > 1 && !cfg.nccl_comm && !cfg.exchange)
+    throw std::invalid_argument("slab over several ranks needs nccl_comm or an exchange callback");
+  for (int k = 0; k < d; ++k)
+    if (desc->axis[k].m == 0) throw std::invalid_argument("slab plans need every m (tune on one rank, broadcast)");
+  P->ax.clear();
+  for (int k = 0; k < d; ++k) P->ax.push_back(make_axis(hb::deriveParams(desc->axis[k].L, desc->axis[k].M, desc->axis[k].m, syms[k])));
+  auto st = std::unique_ptr<SlabState, SlabDel>(new SlabState());
+  st->cfg = cfg;
+  st->ay = P->ax[1];
+  const AxisPlan& ay = st->ay;
+  st->g = hslab::make_geometry(cfg.rank, cfg.nranks, data[0], data[1], d == 3 ? data[2] : 1, (size_t)ay.dev.B,
+                               (size_t)ay.dev.n, 1.0 / (double)ay.dev.qm, cfg.chunks);
+  hconv_desc in{};
+  in.dims = d - 1;
+  in.axis[0] = desc->axis[0];
+  in.axis[0].symmetry = (int)syms[0];
+  if (d == 3) {
+    in.axis[1] = desc->axis[2];
+    in.axis[1].symmetry = (int)syms[2];
+  }
+  in.A = desc->A;
+  in.B = desc->B;
+  in.mult = desc->mult;
+  in.C = std::max<size_t>(1, st->g.max_chunk());
+  in.device = desc->device;
+  in.mult_fn = desc->mult_fn;
+  in.mult_user = desc->mult_user;
+  const hconv_status rc = hconv_plan_create(&in, &st->inner);
+  if (rc != HCONV_OK) {
+    const std::string why = "slab inner plan: " + g_err;
+    if (rc == HCONV_UNSUPPORTED) throw Unsupported(why);
+    if (rc == HCONV_CUDA_ERROR) throw CudaError(why);
+    throw std::invalid_argument(why);
+  }
+  CK(cudaStreamCreateWithFlags(&st->sc, cudaStreamNonBlocking));
+  st->ev.resize(st->g.nchunks);
+  for (auto& e : st->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&st->ev_c, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&st->ev_m, cudaEventDisableTiming));
+  st->ops.st = st.get();
+  st->drv = std::make_unique<hslab::Driver<CudaSlabOps>>(st->g, desc->A, desc->B, st->ops);
+  st->acc.assign(desc->B, nullptr);
+  P->slab = std::move(st);
+}
+
+void slab_convolve(hconv_plan* P, const double2* const* in, double2* const* out, cudaStream_t s) {
+  SlabState& S = *P->slab;
+  const hslab::Geometry& g = S.g;
+  const size_t n = g.nx() * g.Ly * g.Z;
+  std::vector<void*> acc(P->d.B);
+  for (size_t b = 0; b < P->d.B; ++b) {
+    bool alias = false;
+    for (size_t a = 0; a < P->d.A; ++a) alias |= (const void*)out[b] == (const void*)in[a];
+    if (alias) {
+      if (!S.acc[b]) S.acc[b] = (double2*)S.ops.alloc(std::max<size_t>(1, n));
+      acc[b] = S.acc[b];
+    } else {
+      acc[b] = out[b];
+    }
+  }
+  S.ops.s = s;
+  std::vector<const void*> ins(in, in + P->d.A);
+  S.drv->run(ins.data(), acc.data());
+  for (size_t b = 0; b < P->d.B; ++b)
+    if (acc[b] != (void*)out[b] && n) CK(cudaMemcpyAsync(out[b], acc[b], n * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+  CK(cudaGetLastError());
+}
+
 void check_desc(const hconv_desc* d) {
   if (!d) throw std::invalid_argument("null descriptor");
   if (d->dims < 1 || d->dims > 3) throw std::invalid_argument("dims must be 1, 2 or 3");
@@ -993,7 +1297,7 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
   // as many as keep this level's buffers within HCONV_ND_BLOCK_MB (0 = all of them)
   // (B200, c5: chunks of 96 MB 13.7 ms, 1 GB 11.8 ms, unchunked 11.6 ms -- the small per-chunk
   // launches lose more to tails than L2 residency saves -- so blocking is off by default)
-  static const double block_mb = std::getenv("HCONV_ND_BLOCK_MB") ? std::atof(std::getenv("HCONV_ND_BLOCK_MB")) : 0.0;
+  const double block_mb = diag().nd_block_mb;
   P->chunk.assign(d, 1);
   long long NB = (long long)(desc->C ? desc->C : 1);  // arrays at the top level (a batch of N-D arrays)
   for (int l = 0; l < d - 1; ++l) {
@@ -1270,7 +1574,7 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
   return guarded([&] {
     check_desc(desc);
     if (!out) throw std::invalid_argument("null output");
-    CK(cudaSetDevice(desc->device));
+    const DeviceGuard dg(desc->device);
     auto P = std::make_unique<hconv_plan>();
     P->d = *desc;
     P->device = desc->device;
@@ -1287,6 +1591,12 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
       ms[k] = desc->axis[k].m;
       tune |= ms[k] == 0;
     }
+    if (desc->slab) {
+      build_slab(P.get(), syms, data);
+      P->d.slab = nullptr;  // the configuration lives in P->slab (the caller's struct may go)
+      *out = P.release();
+      return;
+    }
     if (tune) {
       if (d == 1) {
         const long long lines = std::min<long long>((long long)(desc->C ? desc->C : 1), 2048);
@@ -1295,8 +1605,45 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
         ms = tune_nd(P.get(), syms, data);
       }
     }
+    if (d == 1 && desc->dist != 0 && desc->dist < data[0])
+      throw std::invalid_argument("dist smaller than the data length: copies would overlap");
     build_plan(P.get(), ms, syms);
     *out = P.release();
+  });
+}
+
+hconv_status hconv_plan_slab(const hconv_plan* p, size_t* x0, size_t* nx) {
+  return guarded([&] {
+    if (!p || !x0 || !nx) throw std::invalid_argument("null argument");
+    if (!p->slab) throw std::invalid_argument("not a slab plan");
+    *x0 = p->slab->g.xs[p->slab->g.rank].lo;
+    *nx = p->slab->g.nx();
+  });
+}
+
+hconv_status hconv_nccl_unique_id(void* id128) {
+  return guarded([&] {
+    if (!id128) throw std::invalid_argument("null argument");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    NC(nccl().GetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+  });
+}
+hconv_status hconv_nccl_comm_init(const void* id128, int nranks, int rank, int device, void** comm) {
+  return guarded([&] {
+    if (!id128 || !comm) throw std::invalid_argument("null argument");
+    const DeviceGuard dg(device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t c = nullptr;
+    NC(nccl().CommInitRank(&c, nranks, id, rank));
+    *comm = c;
+  });
+}
+hconv_status hconv_nccl_comm_destroy(void* comm) {
+  return guarded([&] {
+    if (comm) NC(nccl().CommDestroy((ncclComm_t)comm));
   });
 }
 
@@ -1309,6 +1656,7 @@ hconv_status hconv_plan_params(const hconv_plan* p, int axis, hconv_params* o) {
 
 size_t hconv_plan_workspace_bytes(const hconv_plan* p) {
   if (!p) return 0;
+  if (p->slab) return p->slab->drv->buffer_elems() * sizeof(double2) + hconv_plan_workspace_bytes(p->slab->inner);
   size_t b = p->scratch.bytes;
   const int d = p->d.dims;
   for (int l = 0; l + 1 < d; ++l) {
@@ -1338,9 +1686,11 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
     std::vector<const double2*> ins;
     std::vector<double2*> outs;
     io_arrays(p, in, out, ins, outs);
-    CK(cudaSetDevice(p->device));
+    const DeviceGuard dg(p->device);
     cudaStream_t s = (cudaStream_t)stream;
-    if (p->d.dims == 1) {
+    if (p->slab) {
+      slab_convolve(p, ins.data(), outs.data(), s);
+    } else if (p->d.dims == 1) {
       const AxisPlan& ap = p->ax[0];
       const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
       conv1d(p, ap, (long long)(p->d.C ? p->d.C : 1), dist, ins.data(), outs.data(), s);
@@ -1355,7 +1705,8 @@ hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* con
     std::vector<const double2*> hin_;
     std::vector<double2*> hout_;
     io_arrays(p, in, out, hin_, hout_);
-    CK(cudaSetDevice(p->device));
+    if (p->slab) throw std::invalid_argument("slab plans take device slabs (hconv_convolve)");
+    const DeviceGuard dg(p->device);
     HostPipe& hp = p->host;
     hp.init();
     const size_t A = p->d.A, Bo = p->d.B, W = p->W();
@@ -1365,7 +1716,7 @@ hconv_status hconv_convolve_host(hconv_plan* p, const void* const* in, void* con
       const AxisPlan& ap = p->ax[0];
       const long long C = (long long)(p->d.C ? p->d.C : 1), S = (long long)ap.data;
       const long long dist = (long long)(p->d.dist ? p->d.dist : ap.data);
-      const long long want = std::getenv("HCONV_HOST_CHUNKS") ? std::atoll(std::getenv("HCONV_HOST_CHUNKS")) : 8;
+      const long long want = diag().host_chunks;
       const long long nch = std::max<long long>(1, std::min<long long>(C, want));
       const long long per = (C + nch - 1) / nch;
       hp.ensure((size_t)((per - 1) * dist + S), (int)std::min<long long>(nch, HostPipe::kSlots), W);

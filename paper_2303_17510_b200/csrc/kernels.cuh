@@ -399,6 +399,9 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d(ConvArgs p) {
       HC_TRACE();
       // ---- residue accumulator -> stash (its last reader was the product above)
       if (stage_acc && res > 0) {
+        // the slot was written by this group's generic stores (store_pass0 / store_herm of the
+        // previous residue) and is now read by the async proxy: every writer fences first
+        fence_proxy_async_global();
         sync();
         if (tid == 0) tma_copy(stash, slot, row_bytes, bar_acc);
       }
@@ -633,18 +636,6 @@ __device__ __forceinline__ void acc_tmem_pp(double2 (&v)[Cfg::E], const AxisDev&
 #ifndef HC_PP_TMEM_F
 #define HC_PP_TMEM_F 1
 #endif
-// HC_PP_TMEM_SHARED=1: TMEM stash / accumulator also for kernels with several CTAs per SM when
-// their columns fit together (measured slower for c1's 2048-point plan, 0.039 -> 0.044 ms: off)
-#ifndef HC_PP_TMEM_SHARED
-#define HC_PP_TMEM_SHARED 0
-#endif
-// HC_PP_DIRECT=1: with the accumulator in TMEM, the last residue writes its outputs straight from
-// registers (streaming stores) instead of assembling them in Y for a bulk store, and Y takes the
-// next line's g as soon as the inverse releases it (measured slower on B200: c2 0.795 -> 0.825 ms,
-// c1 0.053 -> 0.056 ms -- the bulk store takes the output traffic off the LSU)
-#ifndef HC_PP_DIRECT
-#define HC_PP_DIRECT 0
-#endif
 // Two line buffers X and Y per group.  X stages f and then serves f's exchanges (and holds the
 // stashed spectrum F), Y stages g and then serves g's and the inverse's exchanges.  The copy of
 // the next f line into X starts as soon as F has been consumed by the product, the next g line
@@ -658,12 +649,10 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
   constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), NBL = Cfg::NB(Cfg::P - 1);
   // tensor memory for the stashed spectrum F and the residue accumulator: kernels whose two
   // line buffers exclude a second CTA on the SM (so the whole TMEM is this CTA's)
-  // (F in TMEM too frees X right after the f transform: c2 0.795 ms vs 0.815 with F in X)
-  // ... or whose TMEM columns fit next to every other CTA shared memory admits on the SM
+  // (F in TMEM too frees X right after the f transform: c2 0.795 ms vs 0.815 with F in X;
+  // sharing TMEM between several CTAs per SM measured slower for c1's 2048-point plan)
   using TLmax = TmemLayout<T * G, Cfg::ES, Cfg::C(0) * Cfg::R(0)>;
-  constexpr int kCtasPerSm = (232448 / 16) / (2 * Cfg::XS * G + Cfg::MT);
-  constexpr bool TM_OK = !STASH_REGS && TLmax::FITS &&
-                         (2 * Cfg::XS * G * 16 > 116 * 1024 || (HC_PP_TMEM_SHARED && TLmax::COLS * kCtasPerSm <= 512));
+  constexpr bool TM_OK = !STASH_REGS && TLmax::FITS && 2 * Cfg::XS * G * 16 > 116 * 1024;
   constexpr bool TM_F = HC_PP_TMEM_F && TM_OK;
   using TL = TmemLayout<T * G, TM_F ? Cfg::ES : 0, Cfg::C(0) * Cfg::R(0)>;
   constexpr bool TMS = HC_PP_TMEM && TM_OK && TL::FITS;
@@ -818,8 +807,9 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
         if (SYM != SYM_HERMITIAN && tid == 0) {
           if (acc_tm) {
             // outputs of a non-final residue go to TMEM: Y is free for the next g line now
-            // (HC_PP_DIRECT: the final residue's too)
-            if ((!last || HC_PP_DIRECT) && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
+            // (writing the final residue straight from registers instead of a bulk store from Y
+            // measured slower: c2 0.795 -> 0.825 ms)
+            if (!last && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
           } else if (acc_y) {
             if constexpr (BULK) bulk_wait_all();  // the slot's bulk store has landed
             tma_copy(Y, slot, row_bytes, bar_g);
@@ -847,46 +837,6 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       if constexpr (SYM == SYM_HERMITIAN) {
         store_herm<Cfg>(v, a, tp, em, res, tid, Y, sync);
         if (tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
-      } else if (BULK && acc_tm && HC_PP_DIRECT && last) {
-        if (!(p.dbg & 1)) {
-          constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1), E0 = C0 * R0;
-          const int L = a.L, H = a.H, LH = L - H, BH = a.B - H;
-          if (res) {
-            const double2* U = tb + (a.oU + res * a.nu);
-            const double2 c1 = tb[a.oC + res * a.nc + 1];
-            sfor<C0>([&](auto Ci) HC_INL {
-              constexpr int c = Ci;
-              sfor<R0>([&](auto Ai) HC_INL {
-                double2 w = cmulc(v[c * R0 + Ai], U[Ai]);
-                if constexpr (SYM == SYM_CENTERED) {
-                  if (Ns1 * Ai + tid + c * Cfg::T >= BH) w = cmul(w, c1);
-                }
-                v[c * R0 + Ai] = w;
-              });
-            });
-            sfor<E0 / 4>([&](auto Ki) HC_INL {
-              double2 t4[4];
-              tm_ld4(ta + 16 * Ki, t4);
-              sfor<4>([&](auto i) HC_INL { v[4 * Ki + i] = cadd(v[4 * Ki + i], t4[i]); });
-            });
-          }
-          double2* out = p.out + base;
-          sfor<C0>([&](auto Ci) HC_INL {
-            constexpr int c = Ci;
-            const int b = tid + c * Cfg::T;
-            if (bvalid<Cfg, 0>(c, tid))
-              sfor<R0>([&](auto Ai) HC_INL {
-                const int s = Ns1 * Ai + b;
-                const double2 w = cscale(v[c * R0 + Ai], em.scale);
-                if constexpr (SYM == SYM_COMPLEX) {
-                  if (s < L) __stcs(out + (long long)s * es, w);
-                } else {
-                  if (s < LH) __stcs(out + (long long)(s + H) * es, w);
-                  else if (s >= BH) __stcs(out + (long long)(s - BH) * es, w);
-                }
-              });
-          });
-        }
       } else if (BULK && acc_tm) {
         if (last) {
           if (!(p.dbg & 1)) {
@@ -926,8 +876,6 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
             if (acc_y) store_pass0_pp<SYM, Cfg, true, false>(v, a, tb, slot, Y, 1.0, res, tid);
             else store_pass0_pp<SYM, Cfg, false, false>(v, a, tb, slot, Y, 1.0, res, tid);
           }
-        } else if (v[0].x == 12345.678) {
-          p.out[0] = v[1];  // keep the work alive
         }
         if (acc_y) {
           sync();  // every thread has read its accumulator values from Y
@@ -1207,97 +1155,7 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp2(ConvArgs p) {
   if (use_tm && threadIdx.x < 32) tmem_dealloc(tm_base, TL::COLS);
 }
 
-// ------------------------------------------------------------- conv1d, paired --
-// For radix plans with at most 16 values per thread: the forward FFTs of f and g run as one
-// interleaved pair (fft_forward_pair) through two exchange buffers X (f) and Y (g); the product
-// needs no stash.  Staging (p.stage == 1): f and g lines are TMA-copied into X and Y; the next
-// g copy starts when the pair releases Y, the next f copy when the inverse releases X.
-template <int SYM, class Cfg, int G>
-__global__ void __launch_bounds__(Cfg::T * G, 1) k_conv1d_pair(ConvArgs p) {
-  extern __shared__ __align__(16) double2 smem[];
-  __shared__ __align__(8) uint64_t bars[2 * G];
-  const int g = threadIdx.x / Cfg::T, tid = threadIdx.x % Cfg::T;
-  double2* tb = smem;
-  const double2* mt = tb;
-  double2* X = smem + p.ax.tabn + g * p.gs;
-  double2* Y = X + Cfg::XS;
-  uint64_t* bar_f = &bars[2 * g];
-  uint64_t* bar_g = &bars[2 * g + 1];
-  const GroupSync sync{g + 1, Cfg::T};
-  const AxisDev& a = p.ax;
-  stage_tables(tb, a, a.tabn);
-  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
-  const bool stage = p.stage == 1;
-  if (stage && tid == 0) {
-    mbar_init(bar_f, 1);
-    mbar_init(bar_g, 1);
-    fence_mbar_init();
-  }
-  sync();
-  uint32_t ph_f = 0, ph_g = 0;
-  const uint32_t row_bytes = (uint32_t)a.S * 16u;
-  const long long es = p.lin.es, step = (long long)gridDim.x * G;
-  double2* slot = p.scratch + (long long)(blockIdx.x * G + g) * a.S;
-  long long item = (long long)blockIdx.x * G + g;
-  if (stage && tid == 0 && item < p.lin.count) {
-    tma_copy(X, p.f + p.lin.base(item), row_bytes, bar_f);
-    tma_copy(Y, p.g + p.lin.base(item), row_bytes, bar_g);
-  }
-  for (; item < p.lin.count; item += step) {
-    const long long base = p.lin.base(item);
-    for (int res = 0; res < a.n; ++res) {
-      const bool last = res == a.n - 1;
-      const bool more = item + step < p.lin.count;
-      const long long nbase = last ? (more ? p.lin.base(item + step) : -1) : base;
-      double2 v[Cfg::E], w[Cfg::E];
-      const P0Res<SYM> p0{&a, tp, res};
-      if (stage) {
-        mbar_wait(bar_f, ph_f);
-        ph_f ^= 1;
-        mbar_wait(bar_g, ph_g);
-        ph_g ^= 1;
-        load_pass0<SYM, Cfg>(v, a, tp, X, 1, res, tid);
-        load_pass0<SYM, Cfg>(w, a, tp, Y, 1, res, tid);
-        sync();
-      } else {
-        load_pass0<SYM, Cfg>(v, a, tp, p.f + base, es, res, tid);
-        load_pass0<SYM, Cfg>(w, a, tp, p.g + base, es, res, tid);
-      }
-      fft_forward_pair<Cfg>(v, w, X, Y, mt, tid, sync, p0, [&]() HC_INL {
-        if (stage && tid == 0 && nbase >= 0) tma_copy(Y, p.g + nbase, row_bytes, bar_g);
-      });
-      constexpr int RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1);
-      sfor<CL>([&](auto Ci) HC_INL {
-        constexpr int c = Ci;
-        if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-          sfor<RL>([&](auto Ki) HC_INL {
-            double2& F = v[c * RL + Ki];
-            const double2 Gv = w[c * RL + Ki];
-            if constexpr (SYM == SYM_HERMITIAN) F = make_double2(F.x * Gv.x, F.y * Gv.y);
-            else F = cmul(F, Gv);
-          });
-      });
-      fft_inverse<Cfg>(v, X, mt, tid, sync, p0, [&]() HC_INL {
-        if (SYM != SYM_HERMITIAN && stage && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
-      });
-      const double2* acc = res > 0 ? slot : nullptr;
-      const Emit em = last ? Emit{p.out + base, es, acc, 1, 1.0 / (double)a.qm, true} : Emit{slot, 1, acc, 1, 1.0, false};
-      if constexpr (SYM == SYM_HERMITIAN) {
-        store_herm<Cfg>(v, a, tp, em, res, tid, X, sync);
-        if (stage && tid == 0 && nbase >= 0) tma_copy(X, p.f + nbase, row_bytes, bar_f);
-      } else {
-        store_pass0<SYM, Cfg>(v, a, tp, em, res, tid);
-      }
-    }
-  }
-}
-
 // --------------------------------------------------------- column-tile pfft --
-// HC_COLS_PREFETCH=1: every round first warms L2 with the rows of its column for the next round
-// (one 16-byte bulk prefetch per row: measured slower, c4 0.51 -> 0.66 ms, so off)
-#ifndef HC_COLS_PREFETCH
-#define HC_COLS_PREFETCH 0
-#endif
 // Outer-axis passes of the N-D driver read columns at a large element stride.  Here the GC
 // line groups of a CTA take GC ADJACENT columns and interleave thread by thread (thread t ->
 // group t % GC), so every load/store instruction of a warp touches GC consecutive columns
@@ -1321,14 +1179,6 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols(FwdArgs p) {
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
     const bool live = item < p.lin.count;
-    // warm L2 with this column's rows of the next round (HBM latency overlaps this round)
-    if (HC_COLS_PREFETCH) {
-      const long long nitem = item + (long long)gridDim.x * GC;
-      if (nitem < p.lin.count) {
-        const double2* src = p.f + p.lin.base(nitem);
-        for (int j = tid; j < a.S; j += T) l2_prefetch(src + (long long)j * p.lin.es, 16);
-      }
-    }
     double2 v[Cfg::E];
     if (live) load_pass0<SYM, Cfg>(v, a, tp, p.f + p.lin.base(item), p.lin.es, p.v, tid);
     fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X, mt, tid, sync, p0);
@@ -1365,13 +1215,6 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols(BwdArgs p) {
   for (long long rd = 0; rd < rounds; ++rd) {
     const long long item = (rd * gridDim.x + blockIdx.x) * GC + g;
     const bool live = item < p.lin.count;
-    if (HC_COLS_PREFETCH) {
-      const long long nitem = item + (long long)gridDim.x * GC;
-      if (nitem < p.lin.count) {
-        const double2* src = (const double2*)p.F + p.lin.base(nitem);
-        for (int j = tid; j < Cfg::N; j += T) l2_prefetch(src + (long long)j * p.lin.es, 16);
-      }
-    }
     double2 v[Cfg::E];
     if (live) {
       const long long ib = p.lin.base(item), ies = p.lin.es;

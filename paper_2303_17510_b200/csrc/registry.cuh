@@ -21,7 +21,6 @@ struct KernelEntry {
   int P = 0, R[4] = {0, 0, 0, 0};  // radix plan (host builds the pass-0 / middle-pass tables from it)
   int mt = 0;                      // middle-pass table entries (FFTCfg::MT)
   int xs = 0, stash = 0;           // exchange buffer / shared-memory stash per group (complex)
-  bool pair = false;               // conv kernel is k_conv1d_pair (two exchange buffers per group)
   const void* convpp2_fn = nullptr;  // paired ping-pong variant (k_conv1d_pp2: complex, L <= B)
   void (*convpp2)(const ConvArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   const void* convpp_fn = nullptr;  // ping-pong variant (k_conv1d_pp)
@@ -62,9 +61,6 @@ constexpr int column_groups_pp() {
 template <int SYM, class Cfg, int G, bool SMEM_STASH = false, int MINB = 1>
 KernelEntry make_entry(const char* radix) {
   constexpr bool SR = Cfg::E <= 16 && !SMEM_STASH;
-  // paired forward FFTs (k_conv1d_pair) measured slower than the stash path on B200 (r01:
-  // c1 0.069 vs 0.057 ms) -- lower occupancy from two exchange buffers; kept selectable.
-  constexpr bool PAIR = false;
   KernelEntry e;
   e.Bc = Cfg::N;
   e.T = Cfg::T;
@@ -76,15 +72,12 @@ KernelEntry make_entry(const char* radix) {
   for (int i = 0; i < Cfg::P; ++i) e.R[i] = Cfg::R(i);
   e.mt = Cfg::MT;
   e.xs = Cfg::XS;
-  e.stash = PAIR ? Cfg::XS : (SR ? 0 : Cfg::N);  // pair: the second exchange buffer Y
-  e.pair = PAIR;
-  if constexpr (PAIR) e.conv_fn = (const void*)k_conv1d_pair<SYM, Cfg, G>;
-  else e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR, MINB>;
+  e.stash = SR ? 0 : Cfg::N;
+  e.conv_fn = (const void*)k_conv1d<SYM, Cfg, G, SR, MINB>;
   e.fwd_fn = (const void*)k_pfft_fwd<SYM, Cfg, G>;
   e.bwd_fn = (const void*)k_pfft_bwd<SYM, Cfg, G>;
   e.conv = [](const ConvArgs& a, int grid, size_t sm, cudaStream_t s) {
-    if constexpr (PAIR) k_conv1d_pair<SYM, Cfg, G><<<grid, Cfg::T * G, sm, s>>>(a);
-    else k_conv1d<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
+    k_conv1d<SYM, Cfg, G, SR, MINB><<<grid, Cfg::T * G, sm, s>>>(a);
   };
   // paired ping-pong (complex): kernels that own the SM with at most 16 last-pass values per
   // thread (B200: 4096-point blocks 0.560 -> 0.484 ms for L = 4000 x 4096 lines; the split

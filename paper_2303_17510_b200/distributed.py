@@ -1,36 +1,17 @@
-"""Slab-decomposed 2D/3D dealiased convolution over several GPUs.
+"""Slab-decomposed 2D/3D dealiased convolution over several GPUs, through the C ABI.
 
 The reference has no distributed code (SPEC.md:512 lists MPI decomposition as a non-goal); this
-is the multi-GPU extension the north star asks for, built on the same C ABI.
-
-Layout: the contiguous arrays [x][y] (2D) or [x][y][z] (3D, z innermost) are split into x-slabs,
-rank g owning rows [x0_g, x1_g).  Because a padded FFT needs its whole axis, the OUTER padded
-transform runs along y, which every rank holds completely; the sharded axis x becomes an inner
-axis after one all-to-all transpose:
-
-  for each residue block r of the y axis (PAPER.md:584-600 with y as the outer axis):
-    1. local forward padded y-FFT of the A inputs, ONE strided launch per input
-       (hconv_pfft_forward_lines), written k-major: F_a[k][x][z], so the k-block destined for
-       rank h is one contiguous run (the all-to-all send buffer needs no packing); each input's
-       exchange is issued asynchronously, so it overlaps the next input's forward (and each
-       output's exchange the previous output's backward)
-    2. all-to-all: rank g receives the spectral y-lines k in [k0_g, k1_g) of every x-slab,
-       [h][k][x_h][z], and places them as T_a[k][x][z] with x complete (G slice copies)
-    3. the (d-1)-D subconvolutions of all nk spectral lines in ONE batched call
-       (hconv_convolve with C = nk; the plan, and with it the multiplication operator, is
-       created once); outputs in place in T_b, b < B
-    4. all-to-all back: the pieces [h][k][x_g][z] land as W_b[k][x][z] (k-major again)
-    5. local inverse padded y-FFT of block r, accumulated into h_b, the last residue scaled by
-       1/(q_y m_y) (hconv_pfft_backward_lines)
-
-The multi-D DFT is separable and the inner subconvolutions are pointwise in the y frequency,
-so this equals the paper's x-outer recursion numerically.  Exactly (A + B) exchanges per
-residue carry L_x x B_y x (inner) values each.  The collective is torch.distributed
-all_to_all_single (NCCL over NVLink on GPUs; gloo on CPU in the tests).
-
-The local compute goes through a Backend bound to a library exporting include/hconv.h: the
-sm_100a library with CUDA tensors (product), or -- in the CPU tests only -- the oracle with host
-tensors, which exercises exactly the same index arithmetic.
+is the multi-GPU extension the north star asks for.  The decomposition itself -- index
+arithmetic, buffers, the schedule and the exchanges -- is native C++ behind the C ABI
+(``hconv_desc.slab``, include/hconv.h; driver csrc/slab.hpp): the global arrays [x][y] (2D) or
+[x][y][z] (3D, z innermost) are split into x-slabs, the outer padded FFT runs along the locally
+complete axis y, and per y residue two all-to-alls bring complete x-lines to every rank for the
+(d-1)-D subconvolutions and back.  This module only
+  * creates the plan (every m given; ``choose_sizes`` tunes on rank 0 and broadcasts),
+  * provides the exchange: an NCCL communicator the library drives itself (CUDA library, G > 1:
+    grouped ncclSend/ncclRecv on its own stream, chunk by chunk against the subconvolutions), or
+    a torch.distributed all-to-all callback (gloo in the CPU tests, where the library is the
+    oracle exporting the same ABI over host memory -- test infrastructure only).
 """
 from __future__ import annotations
 
@@ -38,6 +19,7 @@ import ctypes as C
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -45,7 +27,7 @@ from . import _abi
 
 
 def partition(n: int, parts: int) -> list[tuple[int, int]]:
-    """Balanced contiguous split of range(n) (uneven sizes allowed: 511 = 7*64 + 63)."""
+    """Balanced contiguous split of range(n), the one csrc/slab.hpp uses (511 = 7*64 + 63)."""
     base, extra = divmod(n, parts)
     out, lo = [], 0
     for g in range(parts):
@@ -53,97 +35,6 @@ def partition(n: int, parts: int) -> list[tuple[int, int]]:
         out.append((lo, hi))
         lo = hi
     return out
-
-
-def _lines(count, nin, d_out, d_in, es) -> _abi.Lines:
-    return _abi.Lines(count, nin, d_out, d_in, es)
-
-
-class _LocalPlan:
-    """A convolution plan of the backend's library (owns the operator callback)."""
-
-    def __init__(self, be: "Backend", desc: _abi.Desc, mult):
-        self.be = be
-        fn, self._keep = (None, None) if mult is None else mult._native(host=be.device.type != "cuda")
-        desc.mult_fn = fn
-        h = C.c_void_p()
-        be._check(be.lib.hconv_plan_create(C.byref(desc), C.byref(h)))
-        self.h = h
-        self.A, self.B = desc.A, desc.B
-
-    def convolve(self, ins: Sequence[torch.Tensor], outs: Sequence[torch.Tensor]) -> None:
-        i = (C.c_void_p * len(ins))(*[t.data_ptr() for t in ins])
-        o = (C.c_void_p * len(outs))(*[t.data_ptr() for t in outs])
-        self.be._check(self.be.lib.hconv_convolve(self.h, i, o, self.be.stream_fn()))
-
-    def __del__(self):
-        if getattr(self, "h", None):
-            self.be.lib.hconv_plan_destroy(self.h)
-            self.h = None
-
-
-class Backend:
-    """Local compute through a library exporting the C ABI of include/hconv.h."""
-
-    def __init__(self, lib: C.CDLL, device: torch.device, stream_fn=None):
-        self.lib = lib
-        self.device = device
-        self.stream_fn = stream_fn or (lambda: None)
-
-    def _check(self, st):
-        _abi.check(self.lib, st)
-
-    def params(self, L, M, m, sym) -> _abi.Params:
-        p = _abi.Params()
-        self._check(self.lib.hconv_derive_params(L, M, m, sym, C.byref(p)))
-        return p
-
-    def block_length(self, p: _abi.Params) -> int:
-        return self.lib.hconv_block_length(C.byref(p))
-
-    def forward_lines(self, x: torch.Tensor, p: _abi.Params, r: int, lin: _abi.Lines, F: torch.Tensor,
-                      lout: _abi.Lines) -> None:
-        self._check(self.lib.hconv_pfft_forward_lines(C.byref(p), C.c_void_p(x.data_ptr()), C.byref(lin), r,
-                                                      C.c_void_p(F.data_ptr()), C.byref(lout), self.stream_fn()))
-
-    def backward_lines(self, F: torch.Tensor, p: _abi.Params, r: int, lin: _abi.Lines, h: torch.Tensor,
-                       lout: _abi.Lines, accumulate: bool, scale: float) -> None:
-        self._check(self.lib.hconv_pfft_backward_lines(C.byref(p), C.c_void_p(F.data_ptr()), C.byref(lin), r,
-                                                       C.c_void_p(h.data_ptr()), C.byref(lout), int(accumulate),
-                                                       float(scale), self.stream_fn()))
-
-    def plan(self, axes: Sequence[tuple[int, int, int, int]], copies: int, A: int = 2, B: int = 1,
-             mult=None) -> _LocalPlan:
-        """A plan for `copies` contiguous 1D lines or N-D arrays (product, or `mult`)."""
-        d = _abi.Desc()
-        d.dims = len(axes)
-        for k, (L, M, m, s) in enumerate(axes):
-            d.axis[k] = _abi.Axis(L, M, m, s)
-        d.A, d.B, d.C, d.dist = A, B, copies, 0
-        d.mult = _abi.MULT_PRODUCT if mult is None else mult.kind
-        d.device = (self.device.index or 0) if self.device.type == "cuda" else 0
-        return _LocalPlan(self, d, None if mult is None or mult.kind == _abi.MULT_PRODUCT else mult)
-
-    def convolve(self, axes: Sequence[tuple[int, int, int, int]], f: torch.Tensor, g: torch.Tensor, copies: int = 1,
-                 out: Optional[torch.Tensor] = None) -> torch.Tensor:
-        """hconv_convolve over contiguous arrays (1D: `copies` rows; N-D: one array)."""
-        out = f if out is None else out
-        self.plan(axes, copies).convolve([f, g], [out])
-        return out
-
-
-def cuda_backend(device: Optional[torch.device] = None) -> Backend:
-    from . import hconv
-
-    dev = device or torch.device("cuda", torch.cuda.current_device())
-    return Backend(hconv.lib(), dev, lambda: C.c_void_p(torch.cuda.current_stream(dev).cuda_stream))
-
-
-def _a2a(recv: torch.Tensor, send: torch.Tensor, rsplit: list[int], ssplit: list[int], group, async_op=False):
-    """all_to_all_single on complex data (exchanged as float64 pairs); async_op returns the work
-    handle (NCCL: the exchange runs on NCCL's stream, work.wait() orders the current stream)."""
-    return dist.all_to_all_single(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
-                                  [2 * s for s in rsplit], [2 * s for s in ssplit], group=group, async_op=async_op)
 
 
 @dataclass
@@ -154,111 +45,207 @@ class SlabAxis:
     symmetry: int = _abi.COMPLEX
 
 
-class SlabConvND:
-    """x-slab decomposition of a 2D complex or 3D (complex or Hermitian) convolution.
+def _view(ptr: int, count: int, device: torch.device) -> torch.Tensor:
+    """complex128 tensor over `count` elements at a raw address (no copy)."""
+    if count == 0:
+        return torch.empty(0, dtype=torch.complex128, device=device)
+    if device.type == "cuda":
+        from .hconv import _CudaArray
 
-    axes: [x, y] or [x, y, z]; Hermitian mode = z Hermitian (x, y centered).
-    Every subtransform size m must be given (tune per axis with hconv.tune_nd beforehand).
-    mult: None = builtin product (A = 2, B = 1), else an hconv.MultOperator (A inputs, B outputs).
+        return torch.as_tensor(_CudaArray(ptr, count, False), device=device)
+    arr = np.ctypeslib.as_array(C.cast(C.c_void_p(ptr), C.POINTER(C.c_double)), (2 * count,))
+    return torch.from_numpy(arr.view(np.complex128))
+
+
+class _TorchExchange:
+    """hconv_exchange_fn over torch.distributed: the per-peer segments are packed into one
+    contiguous buffer for all_to_all_single (gloo has no list all-to-all) and unpacked at their
+    displacements.  CUDA pointers: ordered on the library's communication stream."""
+
+    def __init__(self, group, device: torch.device):
+        self.group = group
+        self.device = device
+        self.G = dist.get_world_size(group)
+        self.cb = _abi.ExchangeFn(self._fn)
+        self.error: Optional[str] = None
+
+    def _fn(self, send, sc, sd, recv, rc, rd, user, stream):
+        try:
+            G = self.G
+            sc_, sd_, rc_, rd_ = ([int(a[h]) for h in range(G)] for a in (sc, sd, rc, rd))
+            ctx = (torch.cuda.stream(torch.cuda.ExternalStream(stream, device=self.device))
+                   if self.device.type == "cuda" else _null())
+            with ctx:
+                src = _view(send, max((d + c for d, c in zip(sd_, sc_)), default=0), self.device)
+                dst = _view(recv, max((d + c for d, c in zip(rd_, rc_)), default=0), self.device)
+                packed = torch.cat([src[d:d + c] for d, c in zip(sd_, sc_)]) if sum(sc_) else src[:0].clone()
+                out = torch.empty(sum(rc_), dtype=torch.complex128, device=self.device)
+                dist.all_to_all_single(torch.view_as_real(out).view(-1), torch.view_as_real(packed).view(-1),
+                                       [2 * c for c in rc_], [2 * c for c in sc_], group=self.group)
+                off = 0
+                for d, c in zip(rd_, rc_):
+                    dst[d:d + c].copy_(out[off:off + c])
+                    off += c
+            return 0
+        except Exception as e:  # noqa: BLE001 -- reported as HCONV_NCCL_ERROR by the library
+            self.error = repr(e)
+            return 1
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+class NcclComm:
+    """An NCCL communicator of the CUDA library over the ranks of a torch.distributed group
+    (unique id from rank 0, broadcast through the group)."""
+
+    def __init__(self, group=None, device: Optional[torch.device] = None):
+        from . import hconv
+
+        self.lib = hconv.lib()
+        rank, G = dist.get_rank(group), dist.get_world_size(group)
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _abi.check(self.lib, self.lib.hconv_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        self.h = C.c_void_p()
+        _abi.check(self.lib, self.lib.hconv_nccl_comm_init(uid, G, rank, dev.index or 0, C.byref(self.h)))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.hconv_nccl_comm_destroy(self.h)
+            self.h = None
+
+
+class SlabConvND:
+    """x-slab plan of a 2D complex or 3D (complex or Hermitian) convolution (hconv_desc.slab).
+
+    axes: [x, y] or [x, y, z], every m given; Hermitian mode = z Hermitian (x, y centered,
+    PAPER.md:639-642).  lib: a library exporting include/hconv.h -- the CUDA library (default;
+    device slabs) or, in the CPU tests, the oracle (host slabs).  comm: "nccl" (the library's own
+    NCCL communicator; CUDA, default when G > 1) or an NcclComm to share, "torch" (all-to-all
+    callback over `group`), "none" (one rank: the exchange is a local copy; default at G = 1).
+    mult: None = builtin product (A = 2, B = 1), else an hconv.MultOperator.
     """
 
-    def __init__(self, axes: Sequence[SlabAxis], backend: Backend, group=None, mult=None):
+    def __init__(self, axes: Sequence[SlabAxis], lib: Optional[C.CDLL] = None, group=None, mult=None,
+                 comm: str = "auto", chunks: int = 0, device: Optional[torch.device] = None):
         if len(axes) not in (2, 3):
             raise ValueError("slab decomposition is for 2D and 3D convolutions")
         self.axes = list(axes)
-        self.b = backend
         self.group = group
-        self.G = dist.get_world_size(group)
-        self.rank = dist.get_rank(group)
-        self.mult = mult
+        self.G = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if lib is None:
+            from . import hconv
+
+            lib = hconv.lib()
+        self.lib = lib
+        self.cuda = lib.hconv_backend() == b"cuda-sm_100a"
+        self.device = (device or torch.device("cuda", torch.cuda.current_device())) if self.cuda else torch.device("cpu")
         self.A, self.B = (2, 1) if mult is None else (mult.A, mult.B)
+        self._comm = None
+        self._xch = None
+        s = _abi.Slab()
+        s.rank, s.nranks, s.chunks = self.rank, self.G, chunks
+        if comm == "auto":
+            comm = ("nccl" if self.cuda else "torch") if self.G > 1 else "none"
+        if isinstance(comm, NcclComm) or comm == "nccl":
+            if not self.cuda:
+                raise ValueError("NCCL exchange needs the CUDA library")
+            self._comm = comm if isinstance(comm, NcclComm) else NcclComm(group, self.device)
+            s.nccl_comm = self._comm.h
+        elif comm == "torch":
+            self._xch = _TorchExchange(group, self.device)
+            s.exchange = C.cast(self._xch.cb, C.c_void_p)
+        elif comm != "none" or self.G > 1:
+            raise ValueError(f"comm must be 'nccl', 'torch', an NcclComm (or 'none' at one rank), not {comm!r}")
+        self._slab = s
+        d = _abi.Desc()
+        d.dims = len(axes)
+        for k, a in enumerate(axes):
+            d.axis[k] = _abi.Axis(a.L, a.M, a.m, a.symmetry)
+        d.A, d.B, d.C, d.dist = self.A, self.B, 1, 0
+        d.device = (self.device.index or 0) if self.cuda else 0
+        self._mult_keep = None
+        if mult is None or mult.kind == _abi.MULT_PRODUCT:
+            d.mult = _abi.MULT_PRODUCT
+        else:
+            d.mult = mult.kind
+            fn, self._mult_keep = mult._native(host=not self.cuda)
+            d.mult_fn = fn
+        d.slab = C.cast(C.pointer(s), C.c_void_p)
+        h = C.c_void_p()
+        _abi.check(lib, lib.hconv_plan_create(C.byref(d), C.byref(h)))
+        self.h = h
+        x0, nx = C.c_size_t(), C.c_size_t()
+        _abi.check(lib, lib.hconv_plan_slab(h, C.byref(x0), C.byref(nx)))
+        self.x0, self.nx = x0.value, nx.value
         herm = axes[-1].symmetry == _abi.HERMITIAN
-        if len(axes) == 2 and herm:
-            raise NotImplementedError("2D Hermitian slabs need the outer axis sharded (3 transposes)")
-        self.syms = [(_abi.CENTERED if herm and k < len(axes) - 1 else a.symmetry) for k, a in enumerate(axes)]
-        self.data = [((a.L + 1) // 2 if s == _abi.HERMITIAN else a.L) for a, s in zip(axes, self.syms)]
-        ay = axes[1]
-        self.py = backend.params(ay.L, ay.M, ay.m, self.syms[1])
-        self.By = backend.block_length(self.py)
+        self.data = [((a.L + 1) // 2 if (herm and k == len(axes) - 1) else a.L) for k, a in enumerate(axes)]
         self.xs = partition(self.data[0], self.G)
-        self.ks = partition(self.By, self.G)
-        self.inner = self.data[2] if len(axes) == 3 else 1  # z extent (1 for 2D)
-        k0, k1 = self.ks[self.rank]
-        self.nk = k1 - k0
-        x = (axes[0].L, axes[0].M, axes[0].m, self.syms[0])
-        sub = [x] if len(axes) == 2 else [x, (axes[2].L, axes[2].M, axes[2].m, self.syms[2])]
-        # the (d-1)-D subconvolutions of this rank's nk spectral y-lines: one batched plan
-        self.inner_plan = backend.plan(sub, max(1, self.nk), self.A, self.B, mult) if self.nk else None
 
     def local_shape(self) -> tuple[int, ...]:
-        x0, x1 = self.xs[self.rank]
-        return (x1 - x0, *self.data[1:])
+        return (self.nx, *self.data[1:])
+
+    def params(self, axis: int) -> _abi.Params:
+        p = _abi.Params()
+        _abi.check(self.lib, self.lib.hconv_plan_params(self.h, axis, C.byref(p)))
+        return p
+
+    def workspace_bytes(self) -> int:
+        return int(self.lib.hconv_plan_workspace_bytes(self.h))
 
     def convolve(self, inputs: Sequence[torch.Tensor], out: Optional[Sequence[torch.Tensor]] = None) -> list[torch.Tensor]:
-        """inputs: this rank's x-slabs (local_shape()) of the A inputs; returns the B output
-        slabs (by default written over the first B inputs)."""
+        """inputs: this rank's x-slabs (local_shape()) of the A inputs; returns the B output slabs
+        (by default written over the first B inputs, the reference's in-place convention)."""
         if isinstance(inputs, torch.Tensor):
             raise TypeError("pass a sequence of input slabs")
         if len(inputs) != self.A:
             raise ValueError(f"expected {self.A} input slabs")
         for t in inputs:
-            if tuple(t.shape) != self.local_shape():
-                raise ValueError(f"expected local slabs of shape {self.local_shape()}")
+            if tuple(t.shape) != self.local_shape() or t.dtype != torch.complex128 or not t.is_contiguous():
+                raise ValueError(f"expected contiguous complex128 slabs of shape {self.local_shape()}")
+            if t.device.type != self.device.type:
+                raise ValueError(f"slabs must live on {self.device.type}")
         outs = list(inputs[:self.B]) if out is None else list(out)
         if len(outs) != self.B:
             raise ValueError(f"expected {self.B} output slabs")
-        G, me, Z, By, nk = self.G, self.rank, self.inner, self.By, self.nk
-        nx = inputs[0].shape[0]
-        Ly, Lx = self.data[1], self.data[0]
-        dev, dt = inputs[0].device, inputs[0].dtype
-        nxz = nx * Z
-        lin = _lines(nxz, Z, Ly * Z, 1, Z)        # y-lines (x, z) of an x-slab [nx][Ly][Z]
-        lspec = _lines(nxz, nxz, 0, 1, nxz)       # the same lines k-major: F[k][x][z]
-        send_sizes = [(b - a) * nxz for a, b in self.ks]
-        recv_sizes = [nk * (b - a) * Z for a, b in self.xs]
-        # one spectral / exchange buffer per input and per output: each exchange runs
-        # asynchronously while the next input's forward (or the previous output's backward) computes
-        F = [torch.empty(By * nxz, dtype=dt, device=dev) for _ in range(self.A)]
-        recv = [torch.empty(sum(recv_sizes), dtype=dt, device=dev) for _ in range(self.A)]
-        T = [torch.empty(max(1, nk) * Lx * Z, dtype=dt, device=dev) for _ in range(max(self.A, self.B))]
-        back = [torch.empty(sum(recv_sizes), dtype=dt, device=dev) for _ in range(self.B)]
-        W = [torch.empty(By * nxz, dtype=dt, device=dev) for _ in range(self.B)]
-        # results accumulate in separate buffers when an output aliases an input (inputs are
-        # read by every residue's forward)
-        ins_ptrs = {t.data_ptr() for t in inputs}
-        acc = [torch.empty_like(o) if o.data_ptr() in ins_ptrs else o for o in outs]
-        n_res = self.py.n
-        scale = 1.0 / (self.py.q * self.py.m)
-        for r in range(n_res):
-            works = []
-            for a in range(self.A):
-                self.b.forward_lines(inputs[a], self.py, r, lin, F[a], lspec)
-                works.append(_a2a(recv[a], F[a], recv_sizes, send_sizes, self.group, async_op=True))
-            for a in range(self.A):
-                works[a].wait()
-                Ta = T[a].view(max(1, nk), Lx, Z)
-                off = 0
-                for (xa, xb), sz in zip(self.xs, recv_sizes):
-                    if sz:
-                        Ta[:, xa:xb, :] = recv[a][off:off + sz].view(nk, xb - xa, Z)
-                    off += sz
-            if nk:
-                self.inner_plan.convolve(T[:self.A], T[:self.B])
-            last = r == n_res - 1
-            works = []
-            for b in range(self.B):
-                Tb = T[b].view(max(1, nk), Lx, Z)
-                off = 0
-                for (xa, xb), sz in zip(self.xs, recv_sizes):
-                    if sz:
-                        back[b][off:off + sz].view(nk, xb - xa, Z).copy_(Tb[:, xa:xb, :])
-                    off += sz
-                works.append(_a2a(W[b], back[b], send_sizes, recv_sizes, self.group, async_op=True))
-            for b in range(self.B):
-                works[b].wait()
-                self.b.backward_lines(W[b], self.py, r, lspec, acc[b], lin, accumulate=r > 0,
-                                      scale=scale if last else 1.0)
-        for o, a_ in zip(outs, acc):
-            if o.data_ptr() != a_.data_ptr():
-                o.copy_(a_)
+        i = (C.c_void_p * self.A)(*[t.data_ptr() for t in inputs])
+        o = (C.c_void_p * self.B)(*[t.data_ptr() for t in outs])
+        stream = C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream) if self.cuda else None
+        st = self.lib.hconv_convolve(self.h, i, o, stream)
+        if st != _abi.OK and self._xch is not None and self._xch.error:
+            raise RuntimeError(f"slab exchange failed: {self._xch.error}")
+        _abi.check(self.lib, st)
         return outs
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.hconv_plan_destroy(self.h)
+            self.h = None
+
+
+def choose_sizes(axes: Sequence[tuple[int, int, int]], group=None, device: Optional[torch.device] = None) -> list[int]:
+    """The device-timed planner's m per axis (tune_nd on rank 0's GPU over the whole problem),
+    broadcast so that every rank builds the same plan (the y blocks must agree).
+    axes: [(L, M, symmetry)]."""
+    from . import hconv
+
+    chosen = [None]
+    if not dist.is_initialized() or dist.get_rank(group) == 0:
+        plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, None, hconv.Symmetry(s)) for L, M, s in axes],
+                                device=(device.index or 0) if device is not None else 0)
+        chosen = [[p.m for p in plan.params]]
+        del plan
+    if dist.is_initialized():
+        dist.broadcast_object_list(chosen, src=0, group=group)
+    return list(chosen[0])

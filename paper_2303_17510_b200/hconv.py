@@ -533,6 +533,14 @@ class CapturedConvolution:
     def __init__(self, inputs: Sequence[torch.Tensor], mult: MultOperator, plan: "_Plan", out: Outs = None):
         if mult.kind != _abi.MULT_PRODUCT and mult.apply is not None:
             raise ValueError("a Python multiplication operator cannot be captured in a CUDA graph")
+        if out is None:
+            raise ValueError("CapturedConvolution needs explicit output arrays: in place, the warm-up "
+                             "call would overwrite the inputs and every replay would convolve its own output")
+        outs_ = [out] if isinstance(out, torch.Tensor) else list(out)
+        for o in outs_:
+            for t in inputs:
+                if o.untyped_storage().data_ptr() == t.untyped_storage().data_ptr():
+                    raise ValueError("CapturedConvolution: an output array aliases an input array")
         run = convolve_nd if isinstance(plan, ConvPlanND) else convolve
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())

@@ -1,8 +1,9 @@
-"""The slab decomposition (paper_2303_17510_b200.distributed) on the GPU: NCCL with one rank
-(the whole machine gpurun gives us), CUDA backend -- the strided line passes
-(hconv_pfft_*_lines), the batched N-D convolve and the exchange bookkeeping -- against the
-single-device convolve_nd on the same seeded inputs.  Multi-rank exchanges are covered on CPU
-(tests/test_distributed_cpu.py, gloo, 2 and 3 ranks)."""
+"""The slab plan (hconv_desc.slab, csrc/slab.hpp) of the CUDA library on one GPU -- the y-axis
+passes in k-major layout, the placement copies, the chunked schedule over two streams and the
+inner batched subconvolutions -- against the single-device convolve_nd on the same seeded
+inputs, with each exchange flavour at one rank: none (local copy), the library's own NCCL
+communicator (binding, comm init, grouped calls) and the torch.distributed callback on the
+library's communication stream.  Multi-rank index arithmetic: tests/test_distributed_cpu.py."""
 import os
 import socket
 
@@ -43,9 +44,10 @@ def _worker(port, q):
         sys.path.insert(0, str(repo / "tests"))
         from oracle_lib import rel_l2
         from paper_2303_17510_b200 import hconv
-        from paper_2303_17510_b200.distributed import SlabAxis, SlabConvND, cuda_backend
+        from paper_2303_17510_b200.distributed import NcclComm, SlabAxis, SlabConvND
 
         res = {}
+        comm = NcclComm()
         for name, axes in CASES.items():
             shape = tuple((L + 1) // 2 if s == 2 else L for L, M, m, s in axes)
             f = torch.empty(shape, dtype=torch.complex128, device="cuda")
@@ -57,10 +59,15 @@ def _worker(port, q):
                 hconv.hermitian_symmetrize_boundary(g, [a[0] for a in axes])
             plan = hconv.ConvPlanND([hconv.AxisSpec(L, M, m, hconv.Symmetry(s)) for L, M, m, s in axes])
             ref = hconv.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu().numpy()
-            sc = SlabConvND([SlabAxis(*a) for a in axes], cuda_backend())
-            h = sc.convolve([f.clone(), g.clone()])[0]
-            torch.cuda.synchronize()
-            res[name] = rel_l2(h.cpu().numpy(), ref)
+            for flavour, chunks in (("none", 0), ("nccl", 3), ("torch", 2)):
+                sc = SlabConvND([SlabAxis(*a) for a in axes], comm=comm if flavour == "nccl" else flavour,
+                                chunks=chunks)
+                h = sc.convolve([f.clone(), g.clone()])[0]
+                torch.cuda.synchronize()
+                res[f"{name}_{flavour}"] = rel_l2(h.cpu().numpy(), ref)
+                assert sc.workspace_bytes() > 0
+                del sc
+        del comm
         q.put((res, None))
     except Exception:  # pragma: no cover - reported to the parent
         import traceback
