@@ -196,10 +196,13 @@ class SlabConvND:
     def local_shape(self) -> tuple[int, ...]:
         return (self.nx, *self.data[1:])
 
-    def params(self, axis: int) -> _abi.Params:
+    def params(self, axis: int):
+        """the axis' PlanParams (hconv.PlanParams: m, p, q, n, blockLength(), ...)."""
+        from .hconv import PlanParams
+
         p = _abi.Params()
         _abi.check(self.lib, self.lib.hconv_plan_params(self.h, axis, C.byref(p)))
-        return p
+        return PlanParams._from_c(p)
 
     def workspace_bytes(self) -> int:
         return int(self.lib.hconv_plan_workspace_bytes(self.h))
