@@ -12,8 +12,9 @@ extern "C" {
  * Re, Im = 2u-1, u = (splitmix64(seed*phi + (a<<56 | comp<<55 | (first_index+i))) >> 11) 2^-53. */
 hconv_status hconv_util_fill_uniform(uint64_t seed, uint64_t a, uint64_t first_index, size_t count, void* out,
                                      void* stream);
-/* Planner report of the last tuning done for this plan: rows (m, p, q, n, block, median ms);
- * returns the row count, or -(count+1) when the choice came from the planner cache. */
+/* Planner report of the last tuning done for this plan: rows of 7 doubles (m, p, q, n, block,
+ * median ms, explicit: 1 for the explicit-dealiasing candidate q = 1, m >= M); returns the row
+ * count, or -(count+1) when the choice came from the planner cache. */
 int hconv_plan_report(const hconv_plan* plan, double* out, int cap);
 /* Example native multiplication operators for HCONV_MULT_CALLBACK (device kernels on the
  * library's stream; a template for user operators written in CUDA):

@@ -188,7 +188,7 @@ def cmd_tune(args) -> int:
         if args.show_space:
             for r in rows:
                 print(f"  m={r['m']:6d} p={r['p']:4d} q={r['q']:5d} n={r['n']:4d} block={r['block']:6d} "
-                      f"median_ms={r['median_ms']:.4f}")
+                      f"median_ms={r['median_ms']:.4f}" + (" explicit" if r.get('explicit') else ""))
     return 0
 
 

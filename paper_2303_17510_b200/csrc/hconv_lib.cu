@@ -8,6 +8,7 @@
 //   tune_1d / tune_nd    SPEC.md:518-572, PAPER.md:894-914 (device events replace the CPU clock)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/file.h>
 #include <nccl.h>  // types only: the functions are bound at run time (nccl() below)
 
 #include <algorithm>
@@ -237,7 +238,8 @@ const double2* root_table(size_t N) {
 
 // ----------------------------------------------------------- axis plans -----
 struct AxisPlan {
-  hb::PlanParams pp;
+  hb::PlanParams pp;  // the caller's parameters (m, p, q, n, blockLength as the reference derives them)
+  int split = 1;      // r > 1: block B executes as r sub-blocks B/r (dev.B = B/r, dev.n = r n; make_axis)
   hc::AxisDev dev{};
   const KernelEntry* k = nullptr;
   size_t data = 0;  // values per line (dataLength)
@@ -328,28 +330,56 @@ void build_tables(AxisPlan& ap) {
   a.tab = dp;
 }
 
+// Blocks longer than the largest single-kernel FFT.  Residue block v of the qm-point padded
+// transform, F_{v + n k} (k < B), splits by k = t + r k'' into r sub-blocks of B' = B / r:
+// F_{(v + n t) + (r n) k''} -- residue v + n t of the same qm-point transform with blocks of B'
+// (the unified form of block_io.cuh holds for any block length dividing qm).  So a block of B
+// executes as r sub-blocks: a radix-r decimation-in-frequency first stage followed by B'-point
+// block FFTs, i.e. the same launches as the hybrid plan (m = B', q = r q).  This is how the
+// explicit candidate m >= M (p = q = 1) runs beyond 6144 complex points.
+// Complex data fold any number of chunks; centered / Hermitian blocks fold at most two, so
+// B' >= L / 2 there.  Returns r (1 when B has a kernel), 0 when no split works.
+int split_factor(const hb::PlanParams& pp, bool allow_naive) {
+  const int sym = (int)pp.symmetry;
+  const size_t B = pp.blockLength();
+  if (find_kernel(sym, complex_len(pp), allow_naive)) return 1;
+  for (size_t r = 2; r <= 64 && B / r >= 64; ++r) {
+    if (B % r) continue;
+    const size_t Bs = B / r;
+    if (pp.symmetry == hb::Symmetry::Hermitian && Bs % 2) continue;
+    if (pp.symmetry != hb::Symmetry::Complex && 2 * Bs < pp.L) continue;
+    const int Bc = (int)(pp.symmetry == hb::Symmetry::Hermitian ? Bs / 2 : Bs);
+    if (const KernelEntry* k = find_kernel(sym, Bc, false); k && !k->naive) return (int)r;
+  }
+  return 0;
+}
+
 // Build the device view of one axis; throws Unsupported if no kernel covers the block.
 AxisPlan make_axis(const hb::PlanParams& pp, bool allow_naive = true) {
   AxisPlan ap;
   ap.pp = pp;
   ap.data = pp.dataLength();
-  const size_t B = pp.blockLength(), qm = pp.paddedLength();
-  if (qm != pp.n * B) throw std::logic_error("qm != n B");
+  const size_t qm = pp.paddedLength();
+  if (qm != pp.n * pp.blockLength()) throw std::logic_error("qm != n B");
   if (qm > (size_t)INT32_MAX / 4) throw Unsupported("padded length too large");
   const int sym = (int)pp.symmetry;
-  const int Bc = complex_len(pp);
+  const int r = split_factor(pp, allow_naive);
+  if (r == 0)
+    throw Unsupported("no kernel for block length " + std::to_string(pp.blockLength()) + " (" + hb::name(pp.symmetry) + ")");
+  ap.split = r;
+  const size_t B = pp.blockLength() / (size_t)r;
+  const int Bc = (int)(pp.symmetry == hb::Symmetry::Hermitian && B % 2 == 0 ? B / 2 : B);
   ap.k = find_kernel(sym, Bc, allow_naive);
-  if (!ap.k) throw Unsupported("no kernel for block length " + std::to_string(B) + " (" + hb::name(pp.symmetry) + ")");
   hc::AxisDev& a = ap.dev;
   a.sym = sym;
   a.L = (int)pp.L;
   a.S = (int)pp.dataLength();
   a.B = (int)B;
   a.Bc = Bc;
-  a.n = (int)pp.n;
+  a.n = (int)pp.n * r;
   a.qm = (int)qm;
   a.H = (int)(pp.L / 2);
-  a.pe = (int)pp.interleave();
+  a.pe = r == 1 ? (int)pp.interleave() : 1;
   a.m = (int)pp.m;
   a.tw = root_table((size_t)Bc);
   a.zq = root_table(qm);
@@ -580,6 +610,39 @@ void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
   CK(cudaGetLastError());
 }
 
+// Residue v of the CALLER's plan (public residue-level entry points): with a split block the r
+// sub-blocks v + n t interleave as k = t + r k'' in the caller's block (natural order, which is
+// the reference order whenever p <= 2).
+void residue_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
+                 int ref_order, cudaStream_t s) {
+  if (ap.split == 1) {
+    launch_fwd(ap, lin, lout, f, F, v, ref_order, s);
+    return;
+  }
+  if (ref_order && ap.pp.interleave() > 1) throw Unsupported("reference block order of a split inner block");
+  const int r = ap.split;
+  const size_t esz = ap.dev.sym == hc::SYM_HERMITIAN ? sizeof(double) : sizeof(double2);
+  hc::Lines lo = lout;
+  lo.es *= r;
+  for (int t = 0; t < r; ++t)
+    launch_fwd(ap, lin, lo, f, (char*)F + (size_t)t * (size_t)lout.es * esz, v + (int)ap.pp.n * t, 0, s);
+}
+void residue_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
+                 const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
+  if (ap.split == 1) {
+    launch_bwd(ap, lin, lout, F, dst, acc, scale, v, ref_order, s);
+    return;
+  }
+  if (ref_order && ap.pp.interleave() > 1) throw Unsupported("reference block order of a split inner block");
+  const int r = ap.split;
+  const size_t esz = ap.dev.sym == hc::SYM_HERMITIAN ? sizeof(double) : sizeof(double2);
+  hc::Lines li = lin;
+  li.es *= r;
+  for (int t = 0; t < r; ++t)
+    launch_bwd(ap, li, lout, (const char*)F + (size_t)t * (size_t)lin.es * esz, dst, t == 0 ? acc : dst,
+               t == r - 1 ? scale : 1.0, v + (int)ap.pp.n * t, 0, s);
+}
+
 // --------------------------------------------------------- synthetic data ---
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -611,47 +674,77 @@ struct Candidate {
   size_t m;
   hb::PlanParams pp;
   double ms = 0;
+  size_t exec_B = 0, exec_n = 0;  // the device work: block length and block count after any split
+  bool explicit_ = false;         // the explicit dealiasing candidate (q = 1, m >= M)
 };
 
-// Candidate m values: 7-smooth sizes whose block length has a radix kernel
-// (the direct-sum kernel only for blocks of at most 64 points).  Distinct m with the same
-// (block length, block count) imply identical device work (the p-point pre-DFTs are the first
-// radix stage of the block FFT, block_io.cuh), so each such class is timed once and labelled
-// by its member with the fewest chunks p (then the smaller m).  Timing ties between classes
-// keep the smaller m.  The explicit candidate p = q = 1 is in the scan whenever a
-// kernel covers m >= M.
+// Candidate m values: 7-smooth sizes whose block length has a kernel, directly
+// or split into sub-blocks (make_axis; the direct-sum kernel only for blocks of at most 64
+// points).  Distinct m with the same device work -- the same (sub-)block length and block count
+// -- are one class (the p-point pre-DFTs are the first radix stage of the block FFT, block_io.cuh;
+// a split block is a radix-r first stage), timed once and labelled by its member with the fewest
+// chunks p (then the smaller m).  Timing ties between classes keep the smaller m.
+// The explicit candidate (q = 1, the smallest such m >= M) is always in the list;
+// when its device work is another class's, it carries that class's time.
 std::vector<Candidate> plan_candidates(hb::Symmetry sym, size_t L, size_t M) {
   std::map<std::pair<size_t, size_t>, Candidate> cls;
+  Candidate expl{0, {}, 0};
   const size_t mmax = 4 * M + 8;
   for (size_t m = 1; m <= mmax; ++m) {
     if (!smooth7(m)) continue;
     hb::PlanParams pp = hb::deriveParams(L, M, m, sym);
-    const int Bc = complex_len(pp);
-    const KernelEntry* k = find_kernel((int)sym, Bc, Bc <= 64);
-    if (!k) continue;
-    auto key = std::make_pair(pp.blockLength(), pp.n);
+    const int r = split_factor(pp, complex_len(pp) <= 64);
+    if (r == 0) continue;
+    Candidate c{m, pp, 0, pp.blockLength() / (size_t)r, pp.n * (size_t)r, false};
+    if (pp.q == 1 && m >= M && expl.m == 0) {
+      expl = c;
+      expl.explicit_ = true;
+    }
+    auto key = std::make_pair(c.exec_B, c.exec_n);
     auto it = cls.find(key);
-    if (it == cls.end() || pp.p < it->second.pp.p) cls[key] = Candidate{m, pp, 0};
+    if (it == cls.end() || pp.p < it->second.pp.p) cls[key] = c;
   }
   std::vector<Candidate> out;
-  for (auto& kv : cls) out.push_back(kv.second);
+  bool have_expl = false;
+  for (auto& kv : cls) {
+    if (expl.m && kv.second.m == expl.m) {
+      kv.second.explicit_ = true;
+      have_expl = true;
+    }
+    out.push_back(kv.second);
+  }
+  if (expl.m && !have_expl) out.push_back(expl);  // shares a hybrid class's device work
   std::sort(out.begin(), out.end(), [](const Candidate& a, const Candidate& b) { return a.m < b.m; });
   return out;
 }
 
-std::string plan_cache_key(hb::Symmetry sym, size_t L, size_t M, long long lines) {
-  return dev_info().name + "|" + hb::name(sym) + "|" + std::to_string(L) + "|" + std::to_string(M) + "|" +
-         std::to_string(lines);
+// Planner cache: a line-oriented text file (HCONV_PLAN_CACHE), one record per
+// line, comma-separated: the key fields (kind, L, M, A, B, C, S, placement) plus the device and
+// its SM clock (timings are only comparable on the same device at the same clocks),
+// then the choice (m, D, placement) and the median in nanoseconds.  Advisory locking (flock):
+// shared while reading, exclusive while appending; the last record of a key wins.
+std::string cache_device() {
+  int d = 0, khz = 0;
+  CK(cudaGetDevice(&d));
+  CK(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, d));
+  std::string n = dev_info().name;
+  std::replace(n.begin(), n.end(), ',', ' ');
+  return n + "," + std::to_string(khz / 1000);
+}
+std::string plan_cache_key(const std::string& kind, size_t L, size_t M, size_t A, size_t B, long long C) {
+  return kind + "," + std::to_string(L) + "," + std::to_string(M) + "," + std::to_string(A) + "," +
+         std::to_string(B) + "," + std::to_string(C) + ",1,out-of-place," + cache_device();
 }
 
 struct PlannerCache {
   std::mutex mu;
-  std::map<std::string, std::pair<size_t, double>> mem;  // key -> (m, median ms)
+  std::map<std::string, std::pair<size_t, double>> mem;  // key -> (m, median ns)
   bool loaded = false;
   std::string path() const {
     const char* p = std::getenv("HCONV_PLAN_CACHE");
     return p ? std::string(p) : std::string();
   }
+  static constexpr int kKeyFields = 10;  // kind L M A B C S placement device clock
   void load() {
     if (loaded) return;
     loaded = true;
@@ -659,21 +752,35 @@ struct PlannerCache {
     if (p.empty()) return;
     FILE* f = std::fopen(p.c_str(), "r");
     if (!f) return;
-    char line[1024];
+    flock(fileno(f), LOCK_SH);
+    char line[2048];
     while (std::fgets(line, sizeof line, f)) {
       std::string s(line);
-      const size_t a = s.rfind(','), b = s.rfind(',', a - 1);
-      if (a == std::string::npos || b == std::string::npos) continue;
-      mem[s.substr(0, b)] = {std::strtoull(s.c_str() + b + 1, nullptr, 10), std::strtod(s.c_str() + a + 1, nullptr)};
+      while (!s.empty() && (s.back() == '\n' || s.back() == '\r')) s.pop_back();
+      std::vector<std::string> fl;
+      size_t st = 0;
+      for (size_t i = 0; i <= s.size(); ++i)
+        if (i == s.size() || s[i] == ',') {
+          fl.push_back(s.substr(st, i - st));
+          st = i + 1;
+        }
+      if ((int)fl.size() != kKeyFields + 4) continue;  // + m, D, placement, median_ns
+      std::string key = fl[0];
+      for (int i = 1; i < kKeyFields; ++i) key += "," + fl[i];
+      mem[key] = {std::strtoull(fl[kKeyFields].c_str(), nullptr, 10), std::strtod(fl[kKeyFields + 3].c_str(), nullptr)};
     }
+    flock(fileno(f), LOCK_UN);
     std::fclose(f);
   }
-  void store(const std::string& key, size_t m, double ms) {
-    mem[key] = {m, ms};
+  void store(const std::string& key, size_t m, double ns) {
+    mem[key] = {m, ns};
     const std::string p = path();
     if (p.empty()) return;
     if (FILE* f = std::fopen(p.c_str(), "a")) {
-      std::fprintf(f, "%s,%zu,%.6f\n", key.c_str(), m, ms);
+      flock(fileno(f), LOCK_EX);
+      std::fprintf(f, "%s,%zu,1,out-of-place,%.0f\n", key.c_str(), m, ns);
+      std::fflush(f);
+      flock(fileno(f), LOCK_UN);
       std::fclose(f);
     }
   }
@@ -694,13 +801,19 @@ std::map<std::string, std::vector<Candidate>>& ranked_memo() {
   return m;
 }
 
-// tune_1d on the device: median of 5 timed runs after one warm-up, CUDA events.
+// tune_1d on the device: median of 5 timed runs after one warm-up, CUDA events,
+// over the plan's own batch (capped by memory: three arrays of at most 2 GiB together).
 // The candidates are timed with the fused binary-product convolution; for a general operator
 // (whose residue loop runs the same padded FFTs through work blocks) that timing is the proxy,
 // while tune_nd times the plan's own operator.
 size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanReport* rep) {
   auto& cache = planner_cache();
-  const std::string key = plan_cache_key(sym, L, M, lines);
+  {
+    const size_t data = hb::deriveParams(L, M, 1, sym).dataLength();
+    const long long cap = std::max<long long>(1, (long long)((size_t(2) << 30) / (3 * 16 * data)));
+    lines = std::max<long long>(1, std::min(lines, cap));
+  }
+  const std::string key = plan_cache_key(hb::name(sym), L, M, 2, 1, lines);
   {
     std::lock_guard<std::mutex> lk(cache.mu);
     cache.load();
@@ -732,7 +845,13 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
   const hc::Lines lin{lines, 1, (long long)data, 0, 1};
   size_t best = 0;
   double best_ms = 1e30;
+  std::map<std::pair<size_t, size_t>, double> class_ms;  // device work already timed
   for (auto& c : cands) {
+    auto cit = class_ms.find({c.exec_B, c.exec_n});
+    if (cit != class_ms.end()) {  // the explicit candidate sharing a hybrid class's launches
+      c.ms = cit->second;
+      continue;
+    }
     AxisPlan ap = make_axis(c.pp);
     launch_conv(ap, lin, f, g, o, scratch, 0);
     std::vector<double> t;
@@ -747,6 +866,7 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
     }
     std::sort(t.begin(), t.end());
     c.ms = t[2];
+    class_ms[{c.exec_B, c.exec_n}] = c.ms;
     if (c.ms < best_ms * (1 - 1e-9)) {  // strict improvement; ties keep the smaller m
       best_ms = c.ms;
       best = c.m;
@@ -761,7 +881,7 @@ size_t tune_axis(hb::Symmetry sym, size_t L, size_t M, long long lines, PlanRepo
   if (rep) rep->timed = cands;
   std::lock_guard<std::mutex> lk(cache.mu);
   ranked_memo()[key] = cands;
-  cache.store(key, best, best_ms);
+  cache.store(key, best, best_ms * 1e6);
   return best;
 }
 
@@ -1330,20 +1450,25 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
 std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms, const std::vector<size_t>& data) {
   const hconv_desc* desc = &P->d;
   const int d = desc->dims;
-  std::string key = dev_info().name + "|nd";
+  // one record per axis: kind "nd<k>:<sym L M m of every axis>" (the joint choice depends on all)
+  std::string sig;
   for (int k = 0; k < d; ++k)
-    key += "|" + std::string(hb::name(syms[k])) + ":" + std::to_string(desc->axis[k].L) + ":" +
+    sig += std::string(k ? "/" : "") + hb::name(syms[k]) + ":" + std::to_string(desc->axis[k].L) + ":" +
            std::to_string(desc->axis[k].M) + ":" + std::to_string(desc->axis[k].m);
+  auto axis_key = [&](int k) {
+    return plan_cache_key("nd" + std::to_string(k) + ":" + sig, desc->axis[k].L, desc->axis[k].M, desc->A, desc->B,
+                          (long long)(desc->C ? desc->C : 1));
+  };
   auto& cache = planner_cache();
   {
     std::lock_guard<std::mutex> lk(cache.mu);
     cache.load();
-    auto it = cache.mem.find(key + "|axis0");
+    auto it = cache.mem.find(axis_key(0));
     if (it != cache.mem.end()) {
       std::vector<size_t> ms(d);
       bool ok = true;
       for (int k = 0; k < d; ++k) {
-        auto jt = cache.mem.find(key + "|axis" + std::to_string(k));
+        auto jt = cache.mem.find(axis_key(k));
         if (jt == cache.mem.end()) ok = false;
         else ms[k] = jt->second.first;
       }
@@ -1363,7 +1488,6 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
     long long lines = 1;
     for (int j = 0; j < d; ++j)
       if (j != k) lines *= (long long)data[j];
-    lines = std::min<long long>(lines, 2048);
     PlanReport r;
     const size_t best = tune_axis(syms[k], a.L, a.M, lines, &r);
     options[k].push_back(best);
@@ -1392,6 +1516,7 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
   for (auto& o : options) total *= o.size();
   std::vector<size_t> best(d);
   for (int k = 0; k < d; ++k) best[k] = options[k][0];
+  double best_nd_ms = 0.0;
   if (total > 1) {
     size_t elems = 1;
     for (size_t x : data) elems *= x;
@@ -1440,9 +1565,10 @@ std::vector<size_t> tune_nd(hconv_plan* P, const std::vector<hb::Symmetry>& syms
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     for (double2* a : arrs) cudaFree(a);
+    best_nd_ms = best_ms;
   }
   std::lock_guard<std::mutex> lk(cache.mu);
-  for (int k = 0; k < d; ++k) cache.store(key + "|axis" + std::to_string(k), best[k], 0.0);
+  for (int k = 0; k < d; ++k) cache.store(axis_key(k), best[k], best_nd_ms * 1e6);
   return best;
 }
 
@@ -1524,7 +1650,7 @@ hconv_status hconv_pfft_forward(const hconv_params* pp, const void* f, size_t di
     const long long bl = (long long)p.blockLength();
     const hc::Lines lin{(long long)p.C, 1, (long long)dist, 0, (long long)p.S};
     const hc::Lines lout{(long long)p.C, 1, bl, 0, 1};
-    launch_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 1, (cudaStream_t)stream);
+    residue_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 1, (cudaStream_t)stream);
   });
 }
 hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t residue, void* h, size_t dist,
@@ -1536,8 +1662,8 @@ hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t r
     const long long bl = (long long)p.blockLength();
     const hc::Lines lin{(long long)p.C, 1, bl, 0, 1};
     const hc::Lines lout{(long long)p.C, 1, (long long)dist, 0, (long long)p.S};
-    launch_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, 1.0, (int)residue, 1,
-               (cudaStream_t)stream);
+    residue_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, 1.0, (int)residue, 1,
+                (cudaStream_t)stream);
   });
 }
 
@@ -1554,7 +1680,7 @@ hconv_status hconv_pfft_forward_lines(const hconv_params* pp, const void* f, con
     const hc::Lines lin = to_lines(in), lout = to_lines(out);
     if (lin.count != lout.count) throw std::invalid_argument("line batches differ in count");
     AxisPlan ap = make_axis(p);
-    launch_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 0, (cudaStream_t)stream);
+    residue_fwd(ap, lin, lout, (const double2*)f, F, (int)residue, 0, (cudaStream_t)stream);
   });
 }
 hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, const hconv_lines* in, size_t residue,
@@ -1565,8 +1691,8 @@ hconv_status hconv_pfft_backward_lines(const hconv_params* pp, const void* F, co
     const hc::Lines lin = to_lines(in), lout = to_lines(out);
     if (lin.count != lout.count) throw std::invalid_argument("line batches differ in count");
     AxisPlan ap = make_axis(p);
-    launch_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, scale, (int)residue, 0,
-               (cudaStream_t)stream);
+    residue_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, scale, (int)residue, 0,
+                (cudaStream_t)stream);
   });
 }
 
@@ -1599,7 +1725,7 @@ hconv_status hconv_plan_create(const hconv_desc* desc, hconv_plan** out) {
     }
     if (tune) {
       if (d == 1) {
-        const long long lines = std::min<long long>((long long)(desc->C ? desc->C : 1), 2048);
+        const long long lines = (long long)(desc->C ? desc->C : 1);
         ms[0] = tune_axis(syms[0], desc->axis[0].L, desc->axis[0].M, lines, &P->report);
       } else {
         ms = tune_nd(P.get(), syms, data);
@@ -1782,9 +1908,9 @@ int hconv_plan_report(const hconv_plan* p, double* out, int cap) {
   int k = 0;
   for (const auto& c : p->report.timed) {
     if (k >= cap) break;
-    double* r = out + 6 * k++;
+    double* r = out + 7 * k++;
     r[0] = (double)c.m; r[1] = (double)c.pp.p; r[2] = (double)c.pp.q; r[3] = (double)c.pp.n;
-    r[4] = (double)c.pp.blockLength(); r[5] = c.ms;
+    r[4] = (double)c.pp.blockLength(); r[5] = c.ms; r[6] = c.explicit_ ? 1.0 : 0.0;
   }
   return p->report.cached ? -k - 1 : k;
 }

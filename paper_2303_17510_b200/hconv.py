@@ -322,12 +322,14 @@ class _Plan:
         return lib().hconv_plan_kernel(self._h, axis).decode()
 
     def planner_report(self) -> tuple[list[dict], bool]:
-        buf = (C.c_double * (6 * 256))()
+        W = 7  # hconv_ext.h: (m, p, q, n, block, median ms, explicit) per row
+        buf = (C.c_double * (W * 256))()
         k = lib().hconv_plan_report(self._h, buf, 256)
         cached = k < 0
         k = -k - 1 if cached else k
-        rows = [dict(m=int(buf[6 * i]), p=int(buf[6 * i + 1]), q=int(buf[6 * i + 2]), n=int(buf[6 * i + 3]),
-                     block=int(buf[6 * i + 4]), median_ms=buf[6 * i + 5]) for i in range(k)]
+        rows = [dict(m=int(buf[W * i]), p=int(buf[W * i + 1]), q=int(buf[W * i + 2]), n=int(buf[W * i + 3]),
+                     block=int(buf[W * i + 4]), median_ms=buf[W * i + 5], explicit=bool(buf[W * i + 6]))
+                for i in range(k)]
         return rows, cached
 
     def workspace_bytes(self) -> int:

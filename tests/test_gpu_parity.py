@@ -469,6 +469,59 @@ def test_planner_picks_valid_plan(cuda):
         best = min(r["median_ms"] for r in rows)
         chosen = [r for r in rows if r["m"] == pp.m][0]
         assert chosen["median_ms"] <= best * 1.0000001
+        # the explicit candidate (p = q = 1, m >= M) is always timed, and the choice is
+        # no slower than it
+        expl = [r for r in rows if r["explicit"]]
+        assert len(expl) == 1 and expl[0]["m"] >= 11999 and expl[0]["q"] == 1 and expl[0]["p"] == 1
+        assert chosen["median_ms"] <= expl[0]["median_ms"] * 1.0000001
+
+
+@pytest.mark.parametrize("L,M,sym", [(16383, 24574, 2), (20000, 39999, 0), (511, 766, 1)])
+def test_planner_always_has_explicit_candidate(cuda, L, M, sym):
+    pp, rows, cached = cuda.tune_1d(L, M, cuda.Symmetry(sym), C_=16)
+    if not cached:
+        expl = [r for r in rows if r["explicit"]]
+        assert len(expl) == 1 and expl[0]["m"] >= M and expl[0]["q"] == 1
+
+
+@pytest.mark.parametrize("L,M,m,sym,C_", [(6000, 11999, 12288, 0, 64),      # explicit c2: 12288 = 2 x 6144
+                                           (20000, 39999, None, 0, 16),      # complex L > 12288 (planner)
+                                           (20000, 39999, 12288, 0, 8),      # P2 block 12288, 4 folded chunks
+                                           (16383, 24574, 24576, 2, 16),     # explicit Hermitian c3: 3 x 8192
+                                           (12287, 18430, 18432, 1, 8)])     # explicit centered: 3 x 6144
+def test_split_blocks_vs_oracle(cuda, oracle, L, M, m, sym, C_):
+    """Blocks beyond the largest single-kernel FFT run as r sub-blocks (make_axis split): the
+    explicit candidates of c2 / c3 and complex lines longer than 12288 points."""
+    S = (L + 1) // 2 if sym == 2 else L
+    rng = np.random.default_rng(L + C_)
+    f, g = _rand(rng, (C_, S)), _rand(rng, (C_, S))
+    if sym == 2:
+        f[:, 0], g[:, 0] = f[:, 0].real, g[:, 0].real
+    plan = cuda.Conv1dPlan(L, M, m, cuda.Symmetry(sym), C_=C_)
+    mm = plan.params.m
+    out = cuda.convolve([_t(f), _t(g)], plan.mult, plan, out=_t(f) * 0)[0].cpu().numpy()
+    ref = oracle.convolve([(L, M, mm, sym)], f, g, C_=C_)
+    _check_conv(out, ref, f, g)
+
+
+@pytest.mark.parametrize("L,M,m,sym", [(6000, 11999, 12288, 0), (9000, 17999, 12288, 0), (16383, 24574, 24576, 2),
+                                       (12287, 18430, 18432, 1)])
+def test_split_block_residues_vs_oracle(cuda, oracle, L, M, m, sym):
+    """Residue-level padded FFTs of split blocks (reference order = natural order for p <= 2)."""
+    pp = cuda.deriveParams(L, M, m, cuda.Symmetry(sym))
+    op = oracle.derive(L, M, m, sym)
+    rng = np.random.default_rng(L)
+    S = pp.dataLength()
+    f = _rand(rng, (2, S))
+    if sym == 2:
+        f[:, 0] = f[:, 0].real
+    for r in range(pp.n):
+        F = cuda.forward(_t(f), pp, r).cpu().numpy()
+        for c in range(2):
+            assert rel_l2(F[c], oracle.forward(op, f[c], r)) <= REL
+        h = cuda.backward(_t(F), pp, r).cpu().numpy()
+        for c in range(2):
+            assert rel_l2(h[c], oracle.backward(op, F[c], r)) <= REL
 
 
 def test_errors(cuda):

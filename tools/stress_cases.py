@@ -1,9 +1,13 @@
-"""Small invocations of every kernel family for compute-sanitizer (tools/sanitize.sh).
+"""Stress cases of every kernel family (the synchronisation check in place of compute-sanitizer,
+which this GPU pool does not allow: runs under it have left GPUs needing a reset).
 
-  python tools/sanitize_cases.py <case>      (one case per process: the sanitizer's report is
-                                              per process)
-Each case runs one convolution through the C ABI and checks it against the CPU oracle, so a run
-that "passes" the sanitizer also computed the right numbers."""
+  HCONV_POISON=1 python tools/stress_cases.py [case ...]
+
+Every scratch / work allocation of the library is NaN-filled (HCONV_POISON=1), so a read
+before write (a missing barrier, a TMA copy consumed before its mbarrier phase, a proxy fence
+missing between generic stores and bulk reads) shows up as NaN or as a mismatch; each case runs
+REPEAT times on fresh outputs and must be bit-identical from run to run (races are
+nondeterministic) and within 1e-12 of the CPU oracle."""
 import sys
 from pathlib import Path
 
@@ -18,12 +22,12 @@ from paper_2303_17510_b200 import hconv  # noqa: E402
 
 # name: (kind, axes [(L, M, m, sym)], copies) -- the kernel each one selects
 CASES = {
-    "pp_c2": ("1d", [(6000, 11999, 6144, 0)], 3),        # k_conv1d_pp 16x16x24, TMEM stash + accumulator
-    "pp2_4096": ("1d", [(4000, 7999, 4096, 0)], 3),      # k_conv1d_pp2 (paired forward FFTs)
-    "pp_small": ("1d", [(1024, 2047, 1024, 0)], 5),      # k_conv1d_pp, several CTAs per SM
+    "pp_c2": ("1d", [(6000, 11999, 6144, 0)], 301),       # persistent loop: > 2 lines per CTA        # k_conv1d_pp 16x16x24, TMEM stash + accumulator
+    "pp2_4096": ("1d", [(4000, 7999, 4096, 0)], 301),      # k_conv1d_pp2 (paired forward FFTs)
+    "pp_small": ("1d", [(1024, 2047, 1024, 0)], 2001),      # k_conv1d_pp, several CTAs per SM
     "pp_centered": ("1d", [(1023, 1534, 512, 1)], 3),    # centered ping-pong
-    "single_herm_tmem": ("1d", [(16383, 24574, 8192, 2)], 2),  # k_conv1d Hermitian, TMEM accumulator
-    "single_stage_acc": ("1d", [(6000, 11999, 6144, 0)], 3),   # k_conv1d, accumulator staged by TMA (HCONV_NO_PP=1)
+    "single_herm_tmem": ("1d", [(16383, 24574, 8192, 2)], 150),  # k_conv1d Hermitian, TMEM accumulator
+    "single_stage_acc": ("1d", [(6000, 11999, 6144, 0)], 301),   # k_conv1d, accumulator staged by TMA (HCONV_NO_PP=1)
     "naive": ("1d", [(19, 37, 7, 0)], 4),                # direct-sum kernels
     "cols_2d": ("nd", [(256, 511, 256, 0), (192, 383, 128, 0)], 1),   # column tiles + inner conv
     "cols_3d_herm": ("nd", [(31, 46, 16, 1), (31, 46, 16, 1), (31, 46, 16, 2)], 1),
@@ -32,6 +36,7 @@ CASES = {
 
 
 ENV = {"single_stage_acc": {"HCONV_NO_PP": "1"}}
+REPEAT = 3
 
 
 def run(case):
@@ -69,8 +74,19 @@ def run(case):
         out = hconv.convolve(dev[:2], plan.mult, plan, out=torch.empty_like(dev[0]))[0]
         ref = o.convolve([axes[0]], xs[0], xs[1], C_=C_)
     torch.cuda.synchronize()
-    err = rel_l2(out.cpu().numpy(), ref)
-    print(f"{case}: kernel={plan.kernel(len(axes) - 1)} rel_l2={err:.2e}")
+    first = out.cpu().numpy()
+    err = rel_l2(first, ref)
+    assert np.isfinite(first).all(), "NaN / Inf in the output: a poisoned scratch value was read"
+    for _ in range(REPEAT - 1):  # fresh output arrays, same inputs: bit-identical results
+        if kind == "nd":
+            again = hconv.convolve_nd(dev[:2], plan.mult, plan, out=torch.full_like(dev[0], float("nan")))[0]
+        elif kind == "gen":
+            again = hconv.convolve(dev, mult, plan, out=torch.full_like(dev[0], float("nan")))[0]
+        else:
+            again = hconv.convolve(dev[:2], plan.mult, plan, out=torch.full_like(dev[0], float("nan")))[0]
+        torch.cuda.synchronize()
+        assert np.array_equal(again.cpu().numpy(), first), "results differ between identical runs"
+    print(f"{case}: kernel={plan.kernel(len(axes) - 1)} rel_l2={err:.2e} repeats={REPEAT} bit-identical")
     assert err <= 1e-12, err
 
 
