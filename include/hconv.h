@@ -22,6 +22,7 @@
  *   hconv_symmetry_from_name proj/include/hconv/plan.hpp:28   symmetryFromName
  *   hconv_pfft_forward       SPEC.md:158,176,194,258,276,331,349  forward1/2/Inner[C|H]
  *   hconv_pfft_backward      SPEC.md:167,185,203,267,285,340,358  backward1/2/Inner[C|H]
+ *   hconv_pfft_forward_pair  SPEC.md:212-220                     forward_conjugate_pair
  *   hconv_pfft_*_lines       the same over two-level strided line batches (PAPER.md:584-600
  *                            outer-axis passes; used by the multi-GPU slab driver)
  *   hconv_plan_create        SPEC.md:400-403 Conv1dPlan, SPEC.md:469-472 ConvPlanND,
@@ -108,6 +109,12 @@ hconv_status hconv_pfft_forward(const hconv_params* pp, const void* f, size_t di
                                 void* stream);
 hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t residue, void* h, size_t dist,
                                  int accumulate, void* stream);
+/* forward_conjugate_pair, complex data: the blocks of
+ * residues v and -v from one real / imaginary split of the input, both in the reference order:
+ * Fv[u*m + l] = F_{q l + u n + v}, Fnv[u*m + l] = F_{q l + u n - v} (indices mod qm).
+ * HCONV_INVALID_ARG for v == 0 or 2v == n (self-paired), HCONV_UNSUPPORTED for other kinds. */
+hconv_status hconv_pfft_forward_pair(const hconv_params* pp, const void* f, size_t dist, size_t residue, void* Fv,
+                                     void* Fnv, void* stream);
 
 /* Two-level line batches for the N-D and slab drivers (the strided outer-axis passes of
  * PAPER.md:584-600): line l of a batch starts at element (l / nin) * d_out + (l % nin) * d_in

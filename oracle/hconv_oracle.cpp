@@ -850,6 +850,20 @@ hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t r
 
 // two-level line batches (include/hconv.h hconv_lines): line l starts at
 // (l / nin) * d_out + (l % nin) * d_in, values at stride es
+hconv_status hconv_pfft_forward_pair(const hconv_params* pp, const void* f, size_t dist, size_t residue, void* Fv,
+                                     void* Fnv, void* /*stream*/) {
+  return guarded([&] {
+    Params P = from_abi(pp);
+    if (P.sym != HCONV_COMPLEX) throw std::runtime_error("forward_conjugate_pair: complex data only");
+    if (residue >= P.n) throw std::invalid_argument("residue out of range");
+    const size_t Ls = stored_len(P), bl = block_len(P), C = pp->C;
+    for (size_t c = 0; c < C; ++c) {
+      std::vector<cd> x(Ls);
+      for (size_t j = 0; j < Ls; ++j) x[j] = ((const cd*)f)[c * dist + j * pp->S];
+      forward_conjugate_pair(P, x.data(), residue, (cd*)Fv + c * bl, (cd*)Fnv + c * bl);
+    }
+  });
+}
 static size_t line_base(const hconv_lines& L, size_t l) { return (l / L.nin) * L.d_out + (l % L.nin) * L.d_in; }
 static void check_lines(const hconv_lines* a, const hconv_lines* b) {
   if (!a || !b) throw std::invalid_argument("null line batch");

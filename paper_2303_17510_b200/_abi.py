@@ -95,6 +95,9 @@ PROTOTYPES = {
         C.c_int,
         [C.POINTER(Params), C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p],
     ),
+    "hconv_pfft_forward_pair": (
+        C.c_int, [C.POINTER(Params), C.c_void_p, C.c_size_t, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p],
+    ),
     "hconv_pfft_forward_lines": (
         C.c_int,
         [C.POINTER(Params), C.c_void_p, C.POINTER(Lines), C.c_size_t, C.c_void_p, C.POINTER(Lines), C.c_void_p],

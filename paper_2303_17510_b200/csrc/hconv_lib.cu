@@ -643,6 +643,45 @@ void residue_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout
                t == r - 1 ? scale : 1.0, v + (int)ap.pp.n * t, 0, s);
 }
 
+// ------------------------------------------------ conjugate-pair forward ----
+// forward_conjugate_pair, complex data: one pass over the
+// input forms A_j = zeta_qm^{v j} Re f_j and B_j = i zeta_qm^{v j} Im f_j once and folds both
+// pre-twiddled sequences, W^{(v)} = sum (A + B) and W^{(-v)} = sum (conj A - conj B), modulo B.
+// Their B-point DFTs (the radix kernels, residue 0 of a plain B-point plan) are the blocks
+// F_{v + n k'} and F_{-v + n k'} (PAPER.md's F_{q l + u n + v} and F_{q l + u n - v},
+// k' = p l + u), written in the reference order u m + l.  On the GPU the trick saves a read of
+// f and one twiddle per point, not FP64 work (an FMA complex multiply costs the same 4 DFMA/DMUL
+// as the A/B split), so the fused convolution kernels do not use it.
+__global__ void k_pair_fold(const double2* f, long long dist, long long S, long long C, int L, int B, int qm, int v,
+                            const double2* zq, double2* Wv, double2* Wn) {
+  const long long total = C * (long long)B;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i / B;
+    const int s = (int)(i % B);
+    double2 a = make_double2(0.0, 0.0), b = make_double2(0.0, 0.0);
+    for (int j = s; j < L; j += B) {
+      const double2 x = f[c * dist + (long long)j * S];
+      const double2 w = zq[(int)(((long long)v * j) % qm)];
+      const double2 A = make_double2(w.x * x.x, w.y * x.x);    // zeta^{vj} Re f_j
+      const double2 Bi = make_double2(-w.y * x.y, w.x * x.y);  // i zeta^{vj} Im f_j
+      a = make_double2(a.x + A.x + Bi.x, a.y + A.y + Bi.y);
+      b = make_double2(b.x + A.x - Bi.x, b.y - A.y + Bi.y);    // conj A - conj B
+    }
+    Wv[i] = a;
+    Wn[i] = b;
+  }
+}
+__global__ void k_pair_order(const double2* X, long long C, int B, int pe, int m, double2* Fv, double2* Fn) {
+  const long long total = C * (long long)B;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i / B;
+    const int k = (int)(i % B);
+    const long long o = c * B + (pe > 1 ? (long long)(k % pe) * m + k / pe : k);
+    Fv[o] = X[i];
+    Fn[o] = X[total + i];
+  }
+}
+
 // --------------------------------------------------------- synthetic data ---
 __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
   z += 0x9E3779B97F4A7C15ull;
@@ -687,7 +726,10 @@ struct Candidate {
 // The explicit candidate (q = 1, the smallest such m >= M) is always in the list;
 // when its device work is another class's, it carries that class's time.
 std::vector<Candidate> plan_candidates(hb::Symmetry sym, size_t L, size_t M) {
-  std::map<std::pair<size_t, size_t>, Candidate> cls;
+  // split blocks (r sub-blocks) enter the scan only as the explicit candidate, or when no block
+  // has a kernel of its own (complex L > 12288), and then at most 8-way and the 8 smallest
+  // amounts of device work: a many-way split is the hybrid plan of its sub-block, labelled worse
+  std::map<std::pair<size_t, size_t>, Candidate> cls, split_cls;
   Candidate expl{0, {}, 0};
   const size_t mmax = 4 * M + 8;
   for (size_t m = 1; m <= mmax; ++m) {
@@ -700,9 +742,19 @@ std::vector<Candidate> plan_candidates(hb::Symmetry sym, size_t L, size_t M) {
       expl = c;
       expl.explicit_ = true;
     }
+    if (r > 8) continue;
+    auto& into = r == 1 ? cls : split_cls;
     auto key = std::make_pair(c.exec_B, c.exec_n);
-    auto it = cls.find(key);
-    if (it == cls.end() || pp.p < it->second.pp.p) cls[key] = c;
+    auto it = into.find(key);
+    if (it == into.end() || pp.p < it->second.pp.p) into[key] = c;
+  }
+  if (cls.empty()) {
+    std::vector<Candidate> sp;
+    for (auto& kv : split_cls) sp.push_back(kv.second);
+    std::sort(sp.begin(), sp.end(), [](const Candidate& a, const Candidate& b) {
+      return a.exec_B * a.exec_n < b.exec_B * b.exec_n || (a.exec_B * a.exec_n == b.exec_B * b.exec_n && a.m < b.m);
+    });
+    for (size_t i = 0; i < sp.size() && i < 8; ++i) cls[{sp[i].exec_B, sp[i].exec_n}] = sp[i];
   }
   std::vector<Candidate> out;
   bool have_expl = false;
@@ -1664,6 +1716,34 @@ hconv_status hconv_pfft_backward(const hconv_params* pp, const void* F, size_t r
     const hc::Lines lout{(long long)p.C, 1, (long long)dist, 0, (long long)p.S};
     residue_bwd(ap, lin, lout, F, (double2*)h, accumulate ? (const double2*)h : nullptr, 1.0, (int)residue, 1,
                 (cudaStream_t)stream);
+  });
+}
+
+hconv_status hconv_pfft_forward_pair(const hconv_params* pp, const void* f, size_t dist, size_t residue, void* Fv,
+                                     void* Fnv, void* stream) {
+  return guarded([&] {
+    const hb::PlanParams p = from_abi(pp);
+    if (p.symmetry != hb::Symmetry::Complex) throw Unsupported("forward_conjugate_pair: complex data only (PAPER.md:795-809)");
+    if (residue >= p.n) throw std::invalid_argument("residue out of range");
+    if (residue == 0 || 2 * residue == p.n) throw std::invalid_argument("forward_conjugate_pair: self-paired residue");
+    const long long C = (long long)p.C, B = (long long)p.blockLength();
+    cudaStream_t s = (cudaStream_t)stream;
+    if (C == 0) return;
+    double2* W = nullptr;  // [Wv | Wn] then the transformed [Xv | Xn]
+    CK(cudaMallocAsync(&W, (size_t)(4 * C * B) * sizeof(double2), s));
+    const double2* zq = root_table(p.paddedLength());
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((C * B + 255) / 256, 8LL * dev_info().sms));
+    k_pair_fold<<<blocks, 256, 0, s>>>((const double2*)f, (long long)dist, (long long)p.S, C, (int)p.L, (int)B,
+                                       (int)p.paddedLength(), (int)residue, zq, W, W + C * B);
+    CK(cudaGetLastError());
+    // plain B-point DFTs of the 2C folded lines: residue 0 of the (L = B, M = B, m = B) plan
+    const AxisPlan plain = make_axis(hb::deriveParams((size_t)B, (size_t)B, (size_t)B, hb::Symmetry::Complex));
+    const hc::Lines lin{2 * C, 1, B, 0, 1};
+    residue_fwd(plain, lin, lin, W, W + 2 * C * B, 0, 0, s);
+    k_pair_order<<<blocks, 256, 0, s>>>(W + 2 * C * B, C, (int)B, (int)p.interleave(), (int)p.m, (double2*)Fv,
+                                        (double2*)Fnv);
+    CK(cudaGetLastError());
+    CK(cudaFreeAsync(W, s));
   });
 }
 

@@ -203,6 +203,21 @@ def forward(f: torch.Tensor, params: PlanParams, r: int, out: Optional[torch.Ten
     return out
 
 
+def forward_conjugate_pair(f: torch.Tensor, params: PlanParams, v: int, stream=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """SPEC.md:212-220 forward_conjugate_pair (complex): the residue blocks of v and -v of every
+    row of ``f`` from one real/imaginary split, reference order (F_{q l + u n + v}, F_{q l + u n - v}).
+    ValueError for a self-paired residue (v == 0 or 2v == n)."""
+    f2 = _dev(f).reshape(-1, f.shape[-1])
+    bl = params.blockLength()
+    Fv = torch.empty(f2.shape[0], bl, dtype=torch.complex128, device=f.device)
+    Fn = torch.empty_like(Fv)
+    p = params._c()
+    p.C, p.S = f2.shape[0], 1
+    _check(lib().hconv_pfft_forward_pair(C.byref(p), C.c_void_p(f2.data_ptr()), f2.shape[1], v,
+                                         C.c_void_p(Fv.data_ptr()), C.c_void_p(Fn.data_ptr()), _stream(stream)))
+    return Fv, Fn
+
+
 def backward(F: torch.Tensor, params: PlanParams, r: int, h: Optional[torch.Tensor] = None, accumulate: bool = False,
              stream=None) -> torch.Tensor:
     """Unnormalised inverse of one residue (backward1/2/Inner[C|H]); accumulate adds into h."""

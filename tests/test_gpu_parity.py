@@ -558,3 +558,29 @@ def test_conv1d_edge_shapes(cuda, oracle, L, M, m, sym, C_):
     rows = sorted(set(list(range(min(C_, 3))) + [C_ - 1, C_ // 2]))
     ref = np.stack([oracle.convolve([(L, M, m, sym)], f[c], g[c]) for c in rows])
     _check_conv(out[rows], ref, f[rows], g[rows])
+
+
+@pytest.mark.parametrize("L,M,m", [(12, 36, 3), (20, 61, 4), (6000, 17999, 1536), (4000, 15999, 1024), (5000, 19999, 6144)])
+def test_conjugate_pair_vs_oracle(cuda, oracle, L, M, m):
+    """forward_conjugate_pair on the GPU against the oracle's restatement of
+    PAPER.md:786-831 and against two independent forwards (block v)."""
+    pp = cuda.deriveParams(L, M, m)
+    op = oracle.derive(L, M, m, 0)
+    if pp.n < 3:
+        pytest.skip("no conjugate pair for n < 3")
+    rng = np.random.default_rng(L + m)
+    f = _rand(rng, (3, L))
+    for v in range(1, pp.n):
+        if 2 * v == pp.n:
+            with pytest.raises(ValueError):
+                cuda.forward_conjugate_pair(_t(f), pp, v)
+            continue
+        Fv, Fn = (x.cpu().numpy() for x in cuda.forward_conjugate_pair(_t(f), pp, v))
+        for c in range(3):
+            a, b = oracle.conjugate_pair(op, f[c], v)
+            assert rel_l2(Fv[c], a) <= REL and rel_l2(Fn[c], b) <= REL
+            assert rel_l2(Fv[c], oracle.forward(op, f[c], v)) <= REL
+    with pytest.raises(ValueError):
+        cuda.forward_conjugate_pair(_t(f), pp, 0)
+    with pytest.raises(NotImplementedError):
+        cuda.forward_conjugate_pair(_t(f[:, :9]), cuda.deriveParams(9, 14, 3, cuda.Symmetry.Centered), 1)
