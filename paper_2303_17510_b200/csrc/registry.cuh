@@ -175,6 +175,8 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4, false, 4>("8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4, false, 4>("16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
+  // 384 = 8x8x6: the explicit 768-point Hermitian block of c5's z axis (M = 766)
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 6>, 64>, 1, false, 8>("8x8x6");
   out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, HC_R1024_G, false, HC_R1024_MINB>("16x16x4");
