@@ -7,6 +7,7 @@
 //   ConvPlanND
 //   tune_1d / tune_nd    SPEC.md:518-572, PAPER.md:894-914 (device events replace the CPU clock)
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled (bound through the runtime)
 #include <dlfcn.h>
 #include <sys/file.h>
 #include <nccl.h>  // types only: the functions are bound at run time (nccl() below)
@@ -61,7 +62,7 @@ struct NcclError : std::runtime_error {
 // Diagnostics switches, read once from the environment (HCONV_*; tools/README.md).  None of
 // them is needed in production: the defaults are the measured-best choices.
 struct Diag {
-  bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, sync_mult;
+  bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, no_cols_tma, sync_mult;
   int dbg;
   double general_block_mb, nd_block_mb;
   long long host_chunks;
@@ -77,6 +78,7 @@ struct Diag {
     trace = on("HCONV_TRACE");
     no_cols = on("HCONV_NO_COLS");
     no_cols_pp = on("HCONV_NO_COLS_PP");
+    no_cols_tma = on("HCONV_NO_COLS_TMA");
     sync_mult = on("HCONV_SYNC_MULT");
     dbg = (int)num("HCONV_DBG", 0);
     general_block_mb = num("HCONV_GENERAL_BLOCK_MB", 256.0);
@@ -546,9 +548,72 @@ int cols_pp_tabn(const AxisPlan& ap, int rows, size_t* smem) {
   return tabn;
 }
 
+// ------------------------------------------------- tensor-map column tiles ----
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static const PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)p;
+  }();
+  return fn;
+}
+// 3D map {2 nin float64, rows, count / nin} of a two-level line batch with unit inner distance,
+// box {2 gc, box_rows, 1}; false when the batch does not have that shape.
+bool tile_map(CUtensorMap* map, const void* base, const hc::Lines& l, int rows, int gc, int box_rows) {
+  auto enc = encode_tiled();
+  if (!enc || l.d_in != 1 || l.nin % gc || l.count % l.nin || (reinterpret_cast<uintptr_t>(base) & 15)) return false;
+  const unsigned long long outer = (unsigned long long)(l.count / l.nin);
+  cuuint64_t dims[3] = {(cuuint64_t)(2 * l.nin), (cuuint64_t)rows, (cuuint64_t)outer};
+  const unsigned long long rs = (unsigned long long)l.es * 16ull;
+  const unsigned long long os = outer > 1 ? (unsigned long long)l.d_out * 16ull : rs * (unsigned long long)rows;
+  if (rs % 16 || os % 16 || rs >= (1ull << 40) || os >= (1ull << 40) || rs == 0 || os == 0) return false;
+  cuuint64_t strides[2] = {rs, os};
+  cuuint32_t box[3] = {(cuuint32_t)(2 * gc), (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// smem of the TMA column kernels: tables + two 128-byte-aligned tile buffers of *bufn values
+// (every box row a tensor copy writes or reads lies inside its buffer); 0 = does not fit
+int cols_tma_tabn(const AxisPlan& ap, int rows_in, int box_in, int rows_out, int box_out, size_t* smem, int* bufn) {
+  if (diag().no_cols_tma || !ap.k->fwdct || ap.k->gcp != ap.k->gc) return 0;
+  const int rin = (rows_in + box_in - 1) / box_in * box_in, rout = (rows_out + box_out - 1) / box_out * box_out;
+  const size_t per = ((size_t)ap.k->gcp * (size_t)std::max({ap.k->xs, rows_in, rin, rout}) + 7) & ~(size_t)7;
+  const size_t bufs = 2 * per;
+  if ((bufs + (size_t)ap.k->mt + 8) * sizeof(double2) > kSmemCap) return 0;
+  const size_t room = kSmemCap / sizeof(double2) - bufs - 8;
+  const int tabn = (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
+  *smem = ((size_t)tabn + 8 + bufs) * sizeof(double2);  // + 128 B: the kernel aligns the buffers
+  *bufn = (int)per;
+  return tabn;
+}
+int box_rows_for(int rows) { return rows >= 256 ? 256 : ((rows + 7) / 8) * 8; }
+
 void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
                 int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  if (use_cols(ap, lin) && !ref_order) {
+    const int rows = (int)ap.data, bi = box_rows_for(rows), bo = box_rows_for(ap.dev.Bc);
+    size_t smt = 0;
+    int bufn = 0;
+    const int tt = cols_tma_tabn(ap, rows, bi, ap.dev.Bc, bo, &smt, &bufn);
+    CUtensorMap mi, mo;
+    if (tt > 0 && lout.count % ap.k->gcp == 0 && lout.nin == lin.nin && tile_map(&mi, f, lin, rows, ap.k->gcp, bi) &&
+        tile_map(&mo, F, lout, ap.dev.Bc, ap.k->gcp, bo)) {
+      const int grid = grid_cols(ap.k->fwdct_fn, ap.k, smt, lin.count, ap.k->gcp);
+      hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+      a.ax.tabn = tt;
+      const hc::TileMaps tm{(int)lin.nin, rows, bi, bo, bufn};
+      ap.k->fwdct(a, tm, mi, mo, grid, smt, s);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   size_t smpp = 0;
   int tpp = 0;
   if (use_cols(ap, lin) && !ref_order && (tpp = cols_pp_tabn(ap, (int)ap.data, &smpp)) > 0) {
@@ -581,6 +646,22 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
 void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const void* F, double2* dst,
                 const double2* acc, double scale, int v, int ref_order, cudaStream_t s) {
   if (lin.count == 0) return;
+  if (use_cols(ap, lout) && !ref_order) {
+    const int rows = ap.dev.Bc, bi = box_rows_for(rows);
+    size_t smt = 0;
+    int bufn = 0;
+    const int tt = cols_tma_tabn(ap, rows, bi, rows, bi, &smt, &bufn);
+    CUtensorMap mi;
+    if (tt > 0 && lout.count % ap.k->gcp == 0 && tile_map(&mi, F, lin, rows, ap.k->gcp, bi)) {
+      const int grid = grid_cols(ap.k->bwdct_fn, ap.k, smt, lin.count, ap.k->gcp);
+      hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+      a.ax.tabn = tt;
+      const hc::TileMaps tm{(int)lin.nin, rows, bi, bi, bufn};
+      ap.k->bwdct(a, tm, mi, grid, smt, s);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   size_t smpp = 0;
   int tpp = 0;
   if (use_cols(ap, lout) && !ref_order && (tpp = cols_pp_tabn(ap, ap.dev.Bc, &smpp)) > 0) {

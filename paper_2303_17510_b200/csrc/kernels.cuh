@@ -1349,6 +1349,163 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols_pp(BwdArgs p) 
   cp_async_wait<0>();
 }
 
+// ------------------------------------------ column-tile pfft, tensor-map TMA --
+// The pipelined column tiles with every tile moved by the TMA engine instead of per-thread
+// copies: a 3D tensor map {inner columns, rows, outer} (float64 pairs) describes the strided
+// columns, one thread issues the box loads of the next tile (<= 256 rows per box) onto the
+// buffer's mbarrier, and -- forward -- the finished block is staged in the tile buffer and
+// written back by tensor stores (bulk groups), so neither direction occupies the LSU and the
+// SM computes the next tile while the copies run.  Tiles never straddle an outer index (host:
+// GC divides the inner extent).  Natural block order only.
+__device__ __forceinline__ double2* align_smem128(double2* p) {
+  const uint32_t a = smem_u32(p);
+  return p + (((a + 127u) & ~127u) - a) / 16u;
+}
+struct TileMaps {
+  int inner;           // columns per outer index (nin)
+  int rows_in;         // rows of the input tile (data rows, or the block for the inverse)
+  int box_in, box_out; // rows per tensor box (<= 256) of the input and output maps
+  int bufn;            // complex values per tile buffer (host: >= every box row written or read)
+};
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1)
+    k_pfft_fwd_cols_tma(FwdArgs p, TileMaps tm, const __grid_constant__ CUtensorMap min,
+                        const __grid_constant__ CUtensorMap mout) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  constexpr int N = Cfg::N;
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  const int rows = tm.rows_in;
+  // tensor copies need 128-byte-aligned shared addresses (the dynamic segment follows the static
+  // mbarriers, so align the absolute address; the host adds the slack)
+  double2* buf0 = align_smem128(smem + a.tabn);
+  double2* buf[2] = {buf0, buf0 + tm.bufn};
+  const long long ntiles = p.lin.count / GC;
+  const bool leader = threadIdx.x == 0;
+  const int kBox = tm.box_in;
+  const int nbox_in = (rows + kBox - 1) / kBox;
+  const uint32_t box_bytes = (uint32_t)GC * 16u * (uint32_t)kBox;
+  auto issue = [&](long long t, int b) HC_INL {
+    if (t >= ntiles) return;
+    const long long item = t * GC;
+    const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+    mbar_expect_tx(&bars[b], box_bytes * (uint32_t)nbox_in);
+    for (int r = 0; r < nbox_in; ++r) tma_tensor_load_3d(buf[b] + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
+  };
+  if (leader) {
+    tma_prefetch_map(&min);
+    tma_prefetch_map(&mout);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (leader) issue(blockIdx.x, 0);
+  uint32_t ph[2] = {0, 0};
+  int k = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int b = k & 1;
+    double2* X = buf[b];
+    if (leader) {
+      bulk_wait_read();  // the other buffer's last tensor store has read its block
+      issue(t + gridDim.x, b ^ 1);
+    }
+    mbar_wait(&bars[b], ph[b]);
+    ph[b] ^= 1;
+    double2 v[Cfg::E];
+    load_pass0<SYM, Cfg>(v, a, tp, X + g, GC, p.v, tid);
+    __syncthreads();  // the staged tile is consumed before the first exchange overwrites it
+    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+    __syncthreads();  // the last exchange's reads are done: X takes the block [k][GC]
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { X[(beta + RpL * Ki) * GC + g] = v[c * RL + Ki]; });
+    });
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (leader) {
+      const long long item = t * GC;
+      const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+      for (int r = 0; r * tm.box_out < N; ++r)
+        tma_tensor_store_3d(&mout, c0, r * tm.box_out, c2, X + (size_t)r * tm.box_out * GC);
+      bulk_commit();
+    }
+  }
+  if (leader) bulk_wait_all();
+}
+
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1)
+    k_pfft_bwd_cols_tma(BwdArgs p, TileMaps tm, const __grid_constant__ CUtensorMap min) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  constexpr int N = Cfg::N;
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  double2* buf0 = align_smem128(smem + a.tabn);
+  double2* buf[2] = {buf0, buf0 + tm.bufn};
+  const long long ntiles = p.lin.count / GC;
+  const bool leader = threadIdx.x == 0;
+  const int kBox = tm.box_in;
+  const int nbox = (N + kBox - 1) / kBox;
+  const uint32_t box_bytes = (uint32_t)GC * 16u * (uint32_t)kBox;
+  auto issue = [&](long long t, int b) HC_INL {
+    if (t >= ntiles) return;
+    const long long item = t * GC;
+    const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+    mbar_expect_tx(&bars[b], box_bytes * (uint32_t)nbox);
+    for (int r = 0; r < nbox; ++r) tma_tensor_load_3d(buf[b] + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
+  };
+  if (leader) {
+    tma_prefetch_map(&min);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (leader) issue(blockIdx.x, 0);
+  uint32_t ph[2] = {0, 0};
+  int k = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+    const int b = k & 1;
+    double2* X = buf[b];
+    // the other buffer's exchanges (previous tile) ended at the barrier closing that tile
+    if (leader) issue(t + gridDim.x, b ^ 1);
+    mbar_wait(&bars[b], ph[b]);
+    ph[b] ^= 1;
+    double2 v[Cfg::E];
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { v[c * RL + Ki] = X[(beta + RpL * Ki) * GC + g]; });
+    });
+    __syncthreads();
+    fft_inverse<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+    const long long ob = p.lout.base(t * GC + g);
+    const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
+    store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
+    __syncthreads();  // X (this tile's exchanges) is free before the next issue into it
+  }
+}
+
 // ---------------------------------------------------------------- pfft fwd --
 template <int SYM, class Cfg, int G>
 __global__ void __launch_bounds__(Cfg::T * G, 1) k_pfft_fwd(FwdArgs p) {

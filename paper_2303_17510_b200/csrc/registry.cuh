@@ -36,6 +36,12 @@ struct KernelEntry {
   const void* bwdcp_fn = nullptr;
   void (*fwdcp)(const FwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
   void (*bwdcp)(const BwdArgs&, int grid, size_t smem, cudaStream_t) = nullptr;
+  // the same tiles moved by tensor-map TMA (k_pfft_*_cols_tma; gcp columns per tile)
+  const void* fwdct_fn = nullptr;
+  const void* bwdct_fn = nullptr;
+  void (*fwdct)(const FwdArgs&, const TileMaps&, const CUtensorMap&, const CUtensorMap&, int grid, size_t smem,
+                cudaStream_t) = nullptr;
+  void (*bwdct)(const BwdArgs&, const TileMaps&, const CUtensorMap&, int grid, size_t smem, cudaStream_t) = nullptr;
 };
 
 // column groups per CTA: up to 8 adjacent columns (128 B rows), <= 1024 threads, and the
@@ -119,6 +125,13 @@ KernelEntry make_entry(const char* radix) {
     };
     e.bwdcp = [](const BwdArgs& a, int grid, size_t sm, cudaStream_t s) {
       k_pfft_bwd_cols_pp<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a);
+    };
+    e.fwdct_fn = (const void*)k_pfft_fwd_cols_tma<SYM, Cfg, GP>;
+    e.bwdct_fn = (const void*)k_pfft_bwd_cols_tma<SYM, Cfg, GP>;
+    e.fwdct = [](const FwdArgs& a, const TileMaps& tm, const CUtensorMap& mi, const CUtensorMap& mo, int grid, size_t sm,
+                 cudaStream_t s) { k_pfft_fwd_cols_tma<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a, tm, mi, mo); };
+    e.bwdct = [](const BwdArgs& a, const TileMaps& tm, const CUtensorMap& mi, int grid, size_t sm, cudaStream_t s) {
+      k_pfft_bwd_cols_tma<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a, tm, mi);
     };
   }
   return e;

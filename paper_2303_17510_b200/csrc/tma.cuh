@@ -5,6 +5,7 @@
 // forward FFT (kernels.cuh, STAGE path).  One elected thread per line group issues the copy;
 // every thread of the group waits on the mbarrier phase.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the maps are encoded on the host, hconv_lib.cu)
 #include <cstdint>
 
 // HC_TMA_FENCE=1: a generic->async proxy fence before every bulk load (off by default: every
@@ -131,6 +132,28 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---- tensor-map (cp.async.bulk.tensor) tiles: 3D maps {inner, rows, outer} of float64 ----
+// Load one box at element coordinates (c0, c1, c2) into shared memory, completing on `bar`.
+__device__ __forceinline__ void tma_tensor_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                   uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+// Store one box from shared memory (bulk-group completion; commit with bulk_commit()).
+__device__ __forceinline__ void tma_tensor_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
 }  // namespace hc

@@ -26,3 +26,20 @@ def test_stress_case(cuda, case):
                        text=True, timeout=600, env=env, cwd=REPO)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
     assert "bit-identical" in r.stdout
+
+
+@pytest.mark.parametrize("case", ["cols_2d", "cols_3d_herm", "cols_3d_c5_like"])
+def test_tma_column_tiles_bit_identical(cuda, case, tmp_path):
+    """The tensor-map TMA column kernels move the same tiles as the cp.async kernels: identical
+    arithmetic, so identical bits (HCONV_NO_COLS_TMA=1 selects the cp.async path)."""
+    outs = []
+    for flag in ("0", "1"):
+        env = dict(os.environ, HCONV_NO_COLS_TMA=flag)
+        pre = str(tmp_path / f"o{flag}")
+        r = subprocess.run([sys.executable, str(REPO / "tools" / "stress_cases.py"), "--dump", pre, case],
+                           capture_output=True, text=True, timeout=600, env=env, cwd=REPO)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+        import numpy as np
+
+        outs.append(np.load(f"{pre}_{case}.npy"))
+    assert (outs[0] == outs[1]).all()

@@ -1,6 +1,6 @@
 # full ncu captures of the c5 kernels, summarised on the box (reports are too big to copy back)
 mkdir -p gpurun_out
-CMD="python bench.py --config c5 --m 768,768,1024 --steps 1 --warmup 3 --no-cpu"
+CMD="python bench.py --config c5 --m 768,768,1024 --steps 1 --warmup 3 --no-cpu --single"
 $CMD > /dev/null 2>&1 || exit 1
 cap() {  # name kernel-regex skip
   ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o /tmp/$1 -f $CMD > gpurun_out/ncu_$1.log 2>&1

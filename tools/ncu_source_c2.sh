@@ -1,6 +1,6 @@
 # per-source-line stall attribution of the c2 kernel (ncu source page, SASS view with line info)
 mkdir -p gpurun_out
-CMD="python bench.py --m 6144 --steps 2 --warmup 3 --no-cpu --no-graph"
+CMD="python bench.py --m 6144 --steps 2 --warmup 3 --no-cpu --single --no-graph"
 $CMD > /dev/null 2>&1 || exit 1
 ncu --set full --clock-control none --import-source on -k regex:k_conv1d_pp -s 3 -c 1 -o /tmp/c2src -f $CMD > gpurun_out/ncu_src.log 2>&1
 echo "FULL EXIT $?"

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 declare -A M=([c1]=2048 [c3]=8192 [c4]=4096,2048 [c5]=768,768,1024)
 for c in ${@:-c1 c3 c4 c5}; do
-  CMD="python bench.py --config $c --m ${M[$c]} --steps 1 --warmup 3 --no-cpu"
+  CMD="python bench.py --config $c --m ${M[$c]} --steps 1 --warmup 3 --no-cpu --single"
   $CMD > gpurun_out/plain_$c.json 2> gpurun_out/plain_$c.err || { echo "$c plain failed"; tail -3 gpurun_out/plain_$c.err; continue; }
   echo "$c plain: $(python -c "import json;d=json.load(open('gpurun_out/plain_$c.json'));print(d['ms_per_step'])")"
   ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv --log-file gpurun_out/launches_$c.csv $CMD > gpurun_out/ncu_launches_$c.log 2>&1

@@ -3,7 +3,7 @@
 # top kernel (each ncu pass only after the same command exited 0 without ncu); summarised on the
 # box (the report itself stays there)
 mkdir -p gpurun_out
-CMD="python bench.py --m 6144 --steps 2 --warmup 3 --no-cpu --no-graph"
+CMD="python bench.py --m 6144 --steps 2 --warmup 3 --no-cpu --single --no-graph"
 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || { echo "plain run failed"; tail gpurun_out/prof_plain.err; exit 1; }
 [ -n "$SKIP_LAUNCHES" ] || ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launches.log 2>&1
 echo "LAUNCHES EXIT $?"

@@ -31,6 +31,7 @@ CASES = {
     "naive": ("1d", [(19, 37, 7, 0)], 4),                # direct-sum kernels
     "cols_2d": ("nd", [(256, 511, 256, 0), (192, 383, 128, 0)], 1),   # column tiles + inner conv
     "cols_3d_herm": ("nd", [(31, 46, 16, 1), (31, 46, 16, 1), (31, 46, 16, 2)], 1),
+    "cols_3d_c5_like": ("nd", [(511, 766, 768, 1), (511, 766, 768, 1), (15, 22, 32, 2)], 1),  # c5 x/y tiles
     "general_op": ("gen", [(1000, 1999, 1024, 0)], 3),   # conv1d_general (A = 3 product)
 }
 
@@ -88,9 +89,16 @@ def run(case):
         assert np.array_equal(again.cpu().numpy(), first), "results differ between identical runs"
     print(f"{case}: kernel={plan.kernel(len(axes) - 1)} rel_l2={err:.2e} repeats={REPEAT} bit-identical")
     assert err <= 1e-12, err
+    if DUMP:
+        np.save(f"{DUMP}_{case}.npy", first)
 
+
+DUMP = None
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or list(CASES)
+    args = sys.argv[1:]
+    if args[:1] == ["--dump"]:
+        DUMP, args = args[1], args[2:]
+    names = args or list(CASES)
     for n in names:
         run(n)
