@@ -45,7 +45,7 @@ def test_fill_uniform_matches_oracle(cuda, oracle):
 
 
 # -------------------------------------------------------------- residue level ----
-FAST_BC = [64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6144]
+FAST_BC = [64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6000, 6144]
 
 
 def _residue_cases():
@@ -474,6 +474,8 @@ def test_planner_picks_valid_plan(cuda):
         expl = [r for r in rows if r["explicit"]]
         assert len(expl) == 1 and expl[0]["m"] >= 11999 and expl[0]["q"] == 1 and expl[0]["p"] == 1
         assert chosen["median_ms"] <= expl[0]["median_ms"] * 1.0000001
+        # 7-smooth space: the radix-5 block m = 6000 = L (10x24x25 plan) is timed too
+        assert any(r["m"] == 6000 and r["block"] == 6000 for r in rows)
 
 
 @pytest.mark.parametrize("L,M,sym", [(16383, 24574, 2), (20000, 39999, 0), (511, 766, 1)])
