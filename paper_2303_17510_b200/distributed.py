@@ -66,6 +66,8 @@ class _TorchExchange:
         self.group = group
         self.device = device
         self.G = dist.get_world_size(group)
+        # a gloo group cannot exchange CUDA tensors: stage device segments through host memory
+        self.host_staged = device.type == "cuda" and dist.get_backend(group) == "gloo"
         self.cb = _abi.ExchangeFn(self._fn)
         self.error: Optional[str] = None
 
@@ -79,9 +81,11 @@ class _TorchExchange:
                 src = _view(send, max((d + c for d, c in zip(sd_, sc_)), default=0), self.device)
                 dst = _view(recv, max((d + c for d, c in zip(rd_, rc_)), default=0), self.device)
                 packed = torch.cat([src[d:d + c] for d, c in zip(sd_, sc_)]) if sum(sc_) else src[:0].clone()
-                out = torch.empty(sum(rc_), dtype=torch.complex128, device=self.device)
-                dist.all_to_all_single(torch.view_as_real(out).view(-1), torch.view_as_real(packed).view(-1),
+                xdev = torch.device("cpu") if self.host_staged else self.device
+                out = torch.empty(sum(rc_), dtype=torch.complex128, device=xdev)
+                dist.all_to_all_single(torch.view_as_real(out).view(-1), torch.view_as_real(packed.to(xdev)).view(-1),
                                        [2 * c for c in rc_], [2 * c for c in sc_], group=self.group)
+                out = out.to(self.device)
                 off = 0
                 for d, c in zip(rd_, rc_):
                     dst[d:d + c].copy_(out[off:off + c])

@@ -586,3 +586,29 @@ def test_conjugate_pair_vs_oracle(cuda, oracle, L, M, m):
         cuda.forward_conjugate_pair(_t(f), pp, 0)
     with pytest.raises(NotImplementedError):
         cuda.forward_conjugate_pair(_t(f[:, :9]), cuda.deriveParams(9, 14, 3, cuda.Symmetry.Centered), 1)
+
+
+@pytest.mark.parametrize("axes", [
+    [(31, 46, 48, 1), (31, 46, 48, 1), (31, 46, 48, 2)],     # explicit outer axes
+    [(63, 94, 96, 1), (63, 94, 96, 1), (63, 94, 32, 2)],
+    [(31, 46, 48, 1), (33, 49, 32, 2)],                       # 2D Hermitian
+    [(511, 766, 768, 1), (15, 22, 32, 2)],                    # 2D, 768-point outer columns
+])
+def test_hermitian_explicit_outer_vs_oracle(cuda, oracle, axes):
+    """Hermitian N-D convolutions with explicit (single-residue) outer axes, 2D and 3D, including
+    c5's 768-point outer columns (TMA column tiles): against the oracle."""
+    L = [a[0] for a in axes]
+    shape = tuple(L[:-1]) + ((L[-1] + 1) // 2,)
+    import torch
+
+    f = torch.empty(shape, dtype=torch.complex128, device="cuda")
+    g = torch.empty_like(f)
+    cuda.fill_uniform(f, 5, 0)
+    cuda.fill_uniform(g, 5, 1)
+    cuda.hermitian_symmetrize_boundary(f, L)
+    cuda.hermitian_symmetrize_boundary(g, L)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(a[0], a[1], a[2], cuda.Symmetry(a[3])) for a in axes])
+    assert all(p.n == 1 for p in plan.params[:-1])
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu().numpy()
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    _check_nd(out, oracle.convolve(axes, fn, gn), fn, gn)
