@@ -149,7 +149,7 @@ typedef struct hconv_desc {
                           * (L, or ceil(L/2) for Hermitian -- K-length storage, SURVEY 8(a) note;
                           * not hconv_stored_length).  N-D: must be 0 (contiguous arrays). */
   int device;            /* CUDA ordinal (ignored by the oracle) */
-  int flags;             /* reserved, 0 */
+  int flags;             /* HCONV_FLAG_* (0 = the fastest layout) */
   hconv_mult_fn mult_fn; /* HCONV_MULT_CALLBACK: the operator (else ignored) */
   void* mult_user;       /* passed through to mult_fn */
   const struct hconv_slab* slab; /* NULL: one device holds the whole problem; else x-slab decomposition
@@ -181,6 +181,13 @@ typedef struct hconv_slab {
   void* exchange_user;
   size_t chunks;              /* k-line chunks per exchange (pipelining); 0 = library default */
 } hconv_slab;
+
+/* hconv_desc.flags.  HCONV_FLAG_MIN_MEMORY: N-D plans reuse ONE subconvolution work buffer for
+ * every outer spectral plane in turn ("the upper column is then reused"), so
+ * the work allocation stays within (A+B) p m L^{d-1} complex words (criterion 7);
+ * the default processes every plane of a level in one batched pass (fastest on the GPU, more
+ * work memory). */
+#define HCONV_FLAG_MIN_MEMORY 1
 
 typedef struct hconv_plan hconv_plan;
 

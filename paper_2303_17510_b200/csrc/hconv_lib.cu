@@ -483,7 +483,8 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
   const void* fn = pp2 ? ap.k->convpp2_fn : cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
   const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
-  scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
+  // per-group accumulator slots: only residue loops with more than one block use them
+  if (ap.dev.n > 1) scratch.ensure((size_t)grid * ap.k->G * ap.dev.S * sizeof(double2));
   hc::ConvArgs a{ap.dev, lin, f, g, out, scratch.p, cl.stage, cl.gs, cl.in_off, nullptr, 0};
   a.dbg = diag().dbg;
   // HCONV_DEBUG_SAME_LINE=1: every line reads/writes line 0 (L2-resident timing of the kernel
@@ -1558,6 +1559,7 @@ void build_plan(hconv_plan* P, const std::vector<size_t>& ms, const std::vector<
     const long long per = (long long)(P->W() * P->ax[l].dev.B + desc->B * P->ax[l].data) * inner * (long long)sizeof(double2);
     long long ch = NB;
     if (l > 0 && block_mb > 0) ch = std::max<long long>(1, std::min<long long>(NB, (long long)(block_mb * 1048576.0 / per)));
+    if (l > 0 && (desc->flags & HCONV_FLAG_MIN_MEMORY)) ch = 1;  // one reused buffer per outer plane
     P->chunk[l] = ch;
     const long long work = ch * P->ax[l].dev.B * inner, acc = ch * (long long)P->ax[l].data * inner;
     for (size_t a = 0; a < P->W(); ++a) {

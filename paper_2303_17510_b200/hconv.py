@@ -390,11 +390,17 @@ class AxisSpec:
     symmetry: Symmetry = Symmetry.Complex
 
 
+FLAG_MIN_MEMORY = 1  # include/hconv.h HCONV_FLAG_MIN_MEMORY
+
+
 class ConvPlanND(_Plan):
     """d-dimensional plan; axes[-1] is the contiguous innermost axis.
     Hermitian mode (innermost Hermitian) makes the outer axes centered."""
 
-    def __init__(self, axes: Sequence[AxisSpec], mult: Optional[MultOperator] = None, device: int = 0, C_: int = 1):
+    def __init__(self, axes: Sequence[AxisSpec], mult: Optional[MultOperator] = None, device: int = 0, C_: int = 1,
+                 min_memory: bool = False):
+        """min_memory: reuse one subconvolution work buffer per outer plane (HCONV_FLAG_MIN_MEMORY,
+        the paper's (A+B) p m L^{d-1} work bound) instead of batching every plane."""
         mult = mult or builtin_mult_product(2)
         if not 1 <= len(axes) <= 3:
             raise ValueError("1 to 3 axes")
@@ -403,6 +409,7 @@ class ConvPlanND(_Plan):
         for k, a in enumerate(axes):
             d.axis[k] = _abi.Axis(a.L, a.M, a.m or 0, int(a.symmetry))
         d.A, d.B, d.mult, d.C, d.dist, d.device = mult.A, mult.B, mult.kind, C_, 0, device
+        d.flags = FLAG_MIN_MEMORY if min_memory else 0
         super().__init__(d, mult)
         self.copies = C_
         self.mult = mult

@@ -612,3 +612,37 @@ def test_hermitian_explicit_outer_vs_oracle(cuda, oracle, axes):
     out = cuda.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0].cpu().numpy()
     fn, gn = f.cpu().numpy(), g.cpu().numpy()
     _check_nd(out, oracle.convolve(axes, fn, gn), fn, gn)
+
+
+
+@pytest.mark.parametrize("axes", [
+    [(64, 128, 64, 0), (64, 128, 128, 0)],                    # 2D L=64 M=128
+    [(16, 32, 16, 0), (16, 32, 16, 0), (16, 32, 32, 0)],      # 3D L=16 M=32
+])
+def test_work_memory_bound(cuda, oracle, axes):
+    """SPEC.md:691 criterion 7: with HCONV_FLAG_MIN_MEMORY (one reused subconvolution buffer per
+    outer plane) the plan's whole device work allocation after a convolution is
+    at most 1.25 (A+B) p m L^{d-1} complex words (hconv_work_memory_words), and the result
+    matches the oracle."""
+    import ctypes as C
+
+    import torch
+
+    shape = tuple(a[0] for a in axes)
+    f = torch.empty(shape, dtype=torch.complex128, device="cuda")
+    g = torch.empty_like(f)
+    cuda.fill_uniform(f, 6, 0)
+    cuda.fill_uniform(g, 6, 1)
+    plan = cuda.ConvPlanND([cuda.AxisSpec(*a) for a in axes], min_memory=True)
+    out = cuda.convolve_nd([f, g], plan.mult, plan, out=torch.empty_like(f))[0]
+    torch.cuda.synchronize()
+    words = plan.workspace_bytes() / 16
+    pp = plan.params[0]._c()
+    implicit, explicit_ = C.c_uint64(), C.c_double()
+    L = axes[0][0]
+    assert cuda.lib().hconv_work_memory_words(C.byref(pp), 2, 1, len(axes), L, C.byref(implicit),
+                                                C.byref(explicit_)) == 0
+    assert implicit.value == 3 * pp.p * pp.m * L ** (len(axes) - 1)
+    assert words <= 1.25 * implicit.value, (words, implicit.value)
+    fn, gn = f.cpu().numpy(), g.cpu().numpy()
+    _check_nd(out.cpu().numpy(), oracle.convolve(axes, fn, gn), fn, gn)
