@@ -646,3 +646,29 @@ def test_work_memory_bound(cuda, oracle, axes):
     assert words <= 1.25 * implicit.value, (words, implicit.value)
     fn, gn = f.cpu().numpy(), g.cpu().numpy()
     _check_nd(out.cpu().numpy(), oracle.convolve(axes, fn, gn), fn, gn)
+
+
+def test_planner_tie_break_fake_timer(cuda):
+    """SPEC.md:536,557 (criterion 10): with an injected constant timer every candidate ties and
+    the planner deterministically keeps the smallest m (1D and per axis in N-D)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    repo = Path(__file__).resolve().parents[1]
+    code = ("import json,sys; sys.path.insert(0, '.');"
+            "from paper_2303_17510_b200 import hconv;"
+            "pp, rows, c = hconv.tune_1d(6000, 11999, C_=64);"
+            "nd = hconv.ConvPlanND([hconv.AxisSpec(96, 191, None), hconv.AxisSpec(80, 159, None)]);"
+            "print(json.dumps({'m': pp.m, 'ms': [r['m'] for r in rows], 'nd': [p.m for p in nd.params]}))")
+    outs = []
+    for _ in range(2):
+        env = dict(os.environ, HCONV_PLAN_FAKE_TIMER="1")
+        env.pop("HCONV_PLAN_CACHE", None)
+        r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, cwd=repo, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    assert outs[0]["m"] == min(outs[0]["ms"])
