@@ -1104,8 +1104,9 @@ hconv_status hconv_convolve(hconv_plan* p, const void* const* in, void* const* o
     Mult mu;
     mu.A = p->d.A; mu.B = p->d.B; mu.kind = p->d.mult; mu.fn = p->d.mult_fn; mu.user = p->d.mult_user;
     const size_t A = mu.A, Bo = mu.B;
-    for (size_t a = 0; a < A; ++a) if (!in[a]) throw std::invalid_argument("null input array");
-    for (size_t b = 0; b < Bo; ++b) if (!out[b]) throw std::invalid_argument("null output array");
+    const bool empty = p->slab && p->slab->g.nx() == 0;  // a slab rank without rows: empty arrays
+    for (size_t a = 0; a < A; ++a) if (!in[a] && !empty) throw std::invalid_argument("null input array");
+    for (size_t b = 0; b < Bo; ++b) if (!out[b] && !empty) throw std::invalid_argument("null output array");
     // a user callback is not assumed thread-safe: the oracle calls it from one thread
     const bool par = mu.kind == HCONV_MULT_PRODUCT;
     if (p->slab) {

@@ -1963,12 +1963,14 @@ size_t hconv_plan_workspace_bytes(const hconv_plan* p) {
 static void io_arrays(const hconv_plan* p, const void* const* in, void* const* out, std::vector<const double2*>& ins,
                       std::vector<double2*>& outs) {
   if (!p || !in || !out) throw std::invalid_argument("null argument");
+  // a slab rank may hold no rows (G > L_x): its (empty) arrays may be null
+  const bool empty = p->slab && p->slab->g.nx() == 0;
   for (size_t a = 0; a < p->d.A; ++a) {
-    if (!in[a]) throw std::invalid_argument("null input array");
+    if (!in[a] && !empty) throw std::invalid_argument("null input array");
     ins.push_back((const double2*)in[a]);
   }
   for (size_t b = 0; b < p->d.B; ++b) {
-    if (!out[b]) throw std::invalid_argument("null output array");
+    if (!out[b] && !empty) throw std::invalid_argument("null output array");
     outs.push_back((double2*)out[b]);
   }
 }

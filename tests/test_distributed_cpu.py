@@ -18,6 +18,8 @@ CASES = {
     "3d_complex": [(5, 9, 3, 0), (4, 7, 2, 0), (3, 5, 3, 0)],
     "3d_hermitian": [(7, 11, 4, 1), (7, 11, 2, 1), (7, 11, 4, 2)],
     "3d_hermitian_inner": [(9, 14, 2, 1), (9, 14, 3, 1), (9, 14, 2, 2)],
+    # more ranks than x rows / y spectral rows: some ranks hold no slab rows or no k-rows
+    "2d_tiny": [(2, 3, 2, 0), (4, 7, 2, 0)],
 }
 
 

@@ -16,6 +16,7 @@ CASES = {
     "2d_complex": [(256, 511, 256, 0), (192, 383, 128, 0)],
     "3d_hermitian": [(63, 94, 32, 1), (63, 94, 48, 1), (63, 94, 32, 2)],
     "3d_complex": [(40, 79, 40, 0), (48, 95, 32, 0), (24, 47, 24, 0)],
+    "2d_tiny": [(2, 3, 2, 0), (4, 7, 2, 0)],  # at three ranks some hold no x rows / no k rows
 }
 
 
