@@ -35,6 +35,11 @@ namespace hc {
 void registry_sym0(KernelEntry* out, int* count);
 void registry_sym1(KernelEntry* out, int* count);
 void registry_sym2(KernelEntry* out, int* count);
+// in-place interleaved convolution kernel (conv_ip.cuh, inst_ip.cu), by complex FFT length
+const void* conv_ip_fn(int sym, int Bc);
+size_t conv_ip_smem_bytes(int Bc, int tabn);
+void conv_ip_radices(int Bc, int* P, int* R, int* mt);
+void conv_ip_launch(int Bc, const ConvArgs& a, int grid, size_t smem, cudaStream_t s);
 }  // namespace hc
 
 using hc::KernelEntry;
@@ -63,6 +68,7 @@ struct NcclError : std::runtime_error {
 // them is needed in production: the defaults are the measured-best choices.
 struct Diag {
   bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, no_cols_tma, sync_mult;
+  bool no_ip;       // HCONV_NO_IP=1: never the in-place interleaved kernel (conv_ip.cuh)
   bool fake_timer;  // planner test hook: every candidate times 1 ms
   int dbg;
   double general_block_mb, nd_block_mb;
@@ -73,6 +79,7 @@ struct Diag {
     poison = on("HCONV_POISON");
     no_stage = on("HCONV_NO_STAGE");
     no_pp = on("HCONV_NO_PP");
+    no_ip = on("HCONV_NO_IP");
     pp2 = !(std::getenv("HCONV_PP2") && std::getenv("HCONV_PP2")[0] == '0');
     same_line = on("HCONV_DEBUG_SAME_LINE");
     no_tmacc = on("HCONV_NO_TMACC");
@@ -245,6 +252,8 @@ struct AxisPlan {
   hb::PlanParams pp;  // the caller's parameters (m, p, q, n, blockLength as the reference derives them)
   int split = 1;      // r > 1: block B executes as r sub-blocks B/r (dev.B = B/r, dev.n = r n; make_axis)
   hc::AxisDev dev{};
+  hc::AxisDev dev_ip{};  // the same axis with the tables of the in-place kernel's radix plan (ip_fn set)
+  const void* ip_fn = nullptr;
   const KernelEntry* k = nullptr;
   size_t data = 0;  // values per line (dataLength)
   int tab_full = 0; // table entries the radix kernels use (dev.tabn = the staged prefix)
@@ -263,10 +272,9 @@ int complex_len(const hb::PlanParams& pp) {
 
 // Per-axis tables of the radix kernels (block_io.cuh "table accessors"): every exponent is
 // reduced exactly in 64-bit integers on the host, so the device never computes a modulo.
-void build_tables(AxisPlan& ap) {
-  hc::AxisDev& a = ap.dev;
-  const KernelEntry* k = ap.k;
-  const int R0 = k->R[0], ns1 = a.Bc / R0, n = a.n;
+// (P, R, mt): the radix plan the tables serve -- the registry entry's, or the in-place kernel's
+void build_tables(AxisPlan& ap, hc::AxisDev& a, int P, const int* R, int mt) {
+  const int R0 = R[0], ns1 = a.Bc / R0, n = a.n;
   const long long qm = a.qm, B = a.B, Bc = a.Bc;
   const int nu = 2 * R0 + 1;
   const int nc = std::max<int>(2, (int)((a.L + B - 1) / B) + 1);
@@ -277,7 +285,7 @@ void build_tables(AxisPlan& ap) {
   // residue-indexed tables U C Z H omit row v = 0 (every kernel skips those factors at v = 0):
   // their offsets point one row before the first stored row.
   a.oMT = 0;
-  const int rU = k->mt, rC = rU + (n - 1) * nu, rA = rC + (n - 1) * nc, rZ = rA + ns1, rH = rZ + (n - 1) * ns1;
+  const int rU = mt, rC = rU + (n - 1) * nu, rA = rC + (n - 1) * nc, rZ = rA + ns1, rH = rZ + (n - 1) * ns1;
   a.oU = rU - nu;
   a.oC = rC - nc;
   a.oA = rA;
@@ -289,7 +297,7 @@ void build_tables(AxisPlan& ap) {
   a.tabn = ap.tab_full;
   a.tabfull = ap.tab_full;
   const int total = a.oBh + R0 + 1;
-  auto key = std::make_tuple((int)a.Bc, a.qm, a.B, a.n, nc, (const void*)k);
+  auto key = std::make_tuple((int)a.Bc, a.qm, a.B, a.n, nc, P, R[0], R[1], R[2], R[3]);
   int d = 0;
   CK(cudaGetDevice(&d));
   static std::mutex mu;
@@ -319,14 +327,14 @@ void build_tables(AxisPlan& ap) {
   for (int i = 0; i <= R0; ++i) h[a.oBh + i] = z(B, (long long)ns1 * i);
   // middle passes 1..P-2: omega_{Ns_i}^{b k}
   int o = a.oMT;
-  for (int i = 1; i + 1 < k->P; ++i) {
+  for (int i = 1; i + 1 < P; ++i) {
     long long Nsi = 1, Nsi1 = 1;
-    for (int j = i; j < k->P; ++j) Nsi *= k->R[j];
-    Nsi1 = Nsi / k->R[i];
-    for (int kk = 1; kk < k->R[i]; ++kk)
+    for (int j = i; j < P; ++j) Nsi *= R[j];
+    Nsi1 = Nsi / R[i];
+    for (int kk = 1; kk < R[i]; ++kk)
       for (long long b = 0; b < Nsi1; ++b) h[o++] = z(Nsi, b * kk);
   }
-  if (o != k->mt) throw std::logic_error("table size mismatch");
+  if (o != mt) throw std::logic_error("table size mismatch");
   double2* dp = nullptr;
   CK(cudaMalloc(&dp, (size_t)total * sizeof(double2)));
   CK(cudaMemcpy(dp, h.data(), (size_t)total * sizeof(double2), cudaMemcpyHostToDevice));
@@ -387,7 +395,17 @@ AxisPlan make_axis(const hb::PlanParams& pp, bool allow_naive = true) {
   a.m = (int)pp.m;
   a.tw = root_table((size_t)Bc);
   a.zq = root_table(qm);
-  if (!ap.k->naive) build_tables(ap);
+  if (!ap.k->naive) {
+    build_tables(ap, ap.dev, ap.k->P, ap.k->R, ap.k->mt);
+    if (r == 1 && (ap.ip_fn = hc::conv_ip_fn(sym, Bc))) {
+      int P = 0, R[4] = {0, 0, 0, 0}, mt = 0;
+      hc::conv_ip_radices(Bc, &P, R, &mt);
+      ap.dev_ip = ap.dev;
+      const int full = ap.tab_full;
+      build_tables(ap, ap.dev_ip, P, R, mt);
+      ap.tab_full = full;  // (the registry plan's; dev_ip.tabfull is the in-place kernel's)
+    }
+  }
   return ap;
 }
 
@@ -483,6 +501,20 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   // the paired ping-pong kernel where it exists (complex, L <= B; registry) -- HCONV_PP2=0 disables it
   const bool pp2_on = diag().pp2;
   const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
+  // the in-place interleaved kernel where it exists (complex unit-stride lines, L <= B, every table staged)
+  if (!diag().no_ip && cl.stage == 3 && ap.ip_fn && ap.dev.L <= ap.dev.B && !diag().trace && !diag().dbg) {
+    hc::ConvArgs a{ap.dev_ip, lin, f, g, out, nullptr, 3, 0, 0, nullptr, 0};
+    a.ax.tabn = ap.dev_ip.tabfull;
+    const size_t smem = hc::conv_ip_smem_bytes(ap.dev.Bc, a.ax.tabn);
+    if (smem <= kSmemCap) {
+      const int nb = occupancy(ap.ip_fn, ap.k->T, smem);
+      const int grid = (int)std::max<long long>(1, std::min<long long>(lin.count, (long long)nb * dev_info().sms));
+      if (diag().same_line) a.lin.d_out = 0;
+      hc::conv_ip_launch(ap.dev.Bc, a, grid, smem, s);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
   const void* fn = pp2 ? ap.k->convpp2_fn : cl.stage == 3 ? ap.k->convpp_fn : ap.k->conv_fn;
   const int grid = grid_for(fn, ap.k, cl.smem, lin.count);
   // per-group accumulator slots: only residue loops with more than one block use them
