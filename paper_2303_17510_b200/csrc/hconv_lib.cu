@@ -39,6 +39,8 @@ void registry_sym2(KernelEntry* out, int* count);
 const void* conv_ip_fn(int sym, int Bc);
 size_t conv_ip_smem_bytes(int Bc, int tabn);
 void conv_ip_radices(int Bc, int* P, int* R, int* mt);
+int conv_ip_threads(int Bc);
+int conv_ip_residues(int Bc);
 void conv_ip_launch(int Bc, const ConvArgs& a, int grid, size_t smem, cudaStream_t s);
 }  // namespace hc
 
@@ -502,16 +504,35 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   const bool pp2_on = diag().pp2;
   const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
   // the in-place interleaved kernel where it exists (complex unit-stride lines, L <= B, every table staged)
-  if (!diag().no_ip && cl.stage == 3 && ap.ip_fn && ap.dev.L <= ap.dev.B && !diag().trace && !diag().dbg) {
+  if (!diag().no_ip && cl.stage == 3 && ap.ip_fn && ap.dev.L <= ap.dev.B &&
+      (hc::conv_ip_residues(ap.dev.Bc) == 0 || hc::conv_ip_residues(ap.dev.Bc) == ap.dev.n)) {
     hc::ConvArgs a{ap.dev_ip, lin, f, g, out, nullptr, 3, 0, 0, nullptr, 0};
     a.ax.tabn = ap.dev_ip.tabfull;
+    a.dbg = diag().dbg;
     const size_t smem = hc::conv_ip_smem_bytes(ap.dev.Bc, a.ax.tabn);
     if (smem <= kSmemCap) {
-      const int nb = occupancy(ap.ip_fn, ap.k->T, smem);
+      const int nb = occupancy(ap.ip_fn, hc::conv_ip_threads(ap.dev.Bc), smem);
       const int grid = (int)std::max<long long>(1, std::min<long long>(lin.count, (long long)nb * dev_info().sms));
       if (diag().same_line) a.lin.d_out = 0;
+      unsigned long long* tbuf = nullptr;
+      if (diag().trace) {  // HCONV_TRACE=1: phase timestamps of three warps of CTA 0 (diagnostics)
+        CK(cudaMalloc(&tbuf, 3 * 128 * sizeof(unsigned long long)));
+        CK(cudaMemset(tbuf, 0, 3 * 128 * sizeof(unsigned long long)));
+        a.trace = tbuf;
+      }
       hc::conv_ip_launch(ap.dev.Bc, a, grid, smem, s);
       CK(cudaGetLastError());
+      if (tbuf) {
+        unsigned long long h[3 * 128];
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost));
+        for (int wsel = 0; wsel < 3; ++wsel) {
+          std::fprintf(stderr, "[hconv ip trace warp-slot %d]", wsel);
+          for (int i = 0; i < 128 && h[wsel * 128 + i]; ++i) std::fprintf(stderr, " %llu", h[wsel * 128 + i] - h[0]);
+          std::fprintf(stderr, "\n");
+        }
+        cudaFree(tbuf);
+      }
       return;
     }
   }

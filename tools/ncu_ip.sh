@@ -1,11 +1,9 @@
 #!/bin/bash
-# one full ncu capture of the in-place c2 kernel (after a plain run), summary + per-source-line stalls
+# one full ncu capture of the in-place c2 kernel (after a plain run); the report comes back in gpurun_out/
 mkdir -p gpurun_out
-CMD="python tools/ip_check.py 6000 11999 6144 4096"
+CMD="python tools/ab_conv.py 6000 11999 6144 4096"
 $CMD > gpurun_out/ip_plain.log 2>&1 || { echo plain failed; tail gpurun_out/ip_plain.log; exit 1; }
 tail -1 gpurun_out/ip_plain.log
-ncu --set full --clock-control none --import-source on -k regex:k_conv1d_ip -s 3 -c 1 -o /tmp/ip_conv -f $CMD > gpurun_out/ncu_ip.log 2>&1
-echo "FULL EXIT $?"; tail -2 gpurun_out/ncu_ip.log
-python tools/ncu_summary.py full /tmp/ip_conv.ncu-rep --json gpurun_out/ip_conv_summary.json
-ncu -i /tmp/ip_conv.ncu-rep --page source --csv 2>/dev/null | gzip -c > gpurun_out/ip_conv_source.csv.gz
-ncu -i /tmp/ip_conv.ncu-rep --page raw --csv 2>/dev/null | gzip -c > gpurun_out/ip_conv_raw.csv.gz
+ncu --set full --clock-control none --import-source on -k regex:k_conv1d_ip -s 3 -c 1 -o gpurun_out/ip_conv -f $CMD > gpurun_out/ncu_ip.log 2>&1
+echo "FULL EXIT $?"; tail -2 gpurun_out/ncu_ip.log; ls -la gpurun_out/ip_conv.ncu-rep
+python tools/ncu_summary.py full gpurun_out/ip_conv.ncu-rep --json gpurun_out/ip_conv_summary.json | head -40
