@@ -35,7 +35,7 @@ namespace hc {
 void registry_sym0(KernelEntry* out, int* count);
 void registry_sym1(KernelEntry* out, int* count);
 void registry_sym2(KernelEntry* out, int* count);
-// in-place interleaved convolution kernel (conv_ip.cuh, inst_ip.cu), by complex FFT length
+// in-place two-residue convolution kernel (conv_ip.cuh, inst_ip.cu), by complex FFT length
 const void* conv_ip_fn(int sym, int Bc);
 size_t conv_ip_smem_bytes(int Bc, int tabn);
 void conv_ip_radices(int Bc, int* P, int* R, int* mt);
@@ -70,7 +70,7 @@ struct NcclError : std::runtime_error {
 // them is needed in production: the defaults are the measured-best choices.
 struct Diag {
   bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, no_cols_tma, sync_mult;
-  bool no_ip;       // HCONV_NO_IP=1: never the in-place interleaved kernel (conv_ip.cuh)
+  bool no_ip;       // HCONV_NO_IP=1: never the in-place two-residue kernel (conv_ip.cuh)
   bool fake_timer;  // planner test hook: every candidate times 1 ms
   int dbg;
   double general_block_mb, nd_block_mb;
@@ -503,36 +503,18 @@ void launch_conv(const AxisPlan& ap, const hc::Lines& lin, const double2* f, con
   // the paired ping-pong kernel where it exists (complex, L <= B; registry) -- HCONV_PP2=0 disables it
   const bool pp2_on = diag().pp2;
   const bool pp2 = pp2_on && cl.stage == 3 && ap.k->convpp2 && ap.dev.L <= ap.dev.B;
-  // the in-place interleaved kernel where it exists (complex unit-stride lines, L <= B, every table staged)
-  if (!diag().no_ip && cl.stage == 3 && ap.ip_fn && ap.dev.L <= ap.dev.B &&
-      (hc::conv_ip_residues(ap.dev.Bc) == 0 || hc::conv_ip_residues(ap.dev.Bc) == ap.dev.n)) {
+  // the in-place two-residue kernel where it exists (complex unit-stride lines, L <= B, n = 2, every table staged)
+  if (!diag().no_ip && cl.stage == 3 && ap.ip_fn && ap.dev.L <= ap.dev.B && ap.dev.n == hc::conv_ip_residues(ap.dev.Bc) &&
+      !diag().trace && !diag().dbg) {
     hc::ConvArgs a{ap.dev_ip, lin, f, g, out, nullptr, 3, 0, 0, nullptr, 0};
     a.ax.tabn = ap.dev_ip.tabfull;
-    a.dbg = diag().dbg;
     const size_t smem = hc::conv_ip_smem_bytes(ap.dev.Bc, a.ax.tabn);
     if (smem <= kSmemCap) {
       const int nb = occupancy(ap.ip_fn, hc::conv_ip_threads(ap.dev.Bc), smem);
       const int grid = (int)std::max<long long>(1, std::min<long long>(lin.count, (long long)nb * dev_info().sms));
       if (diag().same_line) a.lin.d_out = 0;
-      unsigned long long* tbuf = nullptr;
-      if (diag().trace) {  // HCONV_TRACE=1: phase timestamps of three warps of CTA 0 (diagnostics)
-        CK(cudaMalloc(&tbuf, 3 * 128 * sizeof(unsigned long long)));
-        CK(cudaMemset(tbuf, 0, 3 * 128 * sizeof(unsigned long long)));
-        a.trace = tbuf;
-      }
       hc::conv_ip_launch(ap.dev.Bc, a, grid, smem, s);
       CK(cudaGetLastError());
-      if (tbuf) {
-        unsigned long long h[3 * 128];
-        CK(cudaStreamSynchronize(s));
-        CK(cudaMemcpy(h, tbuf, sizeof h, cudaMemcpyDeviceToHost));
-        for (int wsel = 0; wsel < 3; ++wsel) {
-          std::fprintf(stderr, "[hconv ip trace warp-slot %d]", wsel);
-          for (int i = 0; i < 128 && h[wsel * 128 + i]; ++i) std::fprintf(stderr, " %llu", h[wsel * 128 + i] - h[0]);
-          std::fprintf(stderr, "\n");
-        }
-        cudaFree(tbuf);
-      }
       return;
     }
   }
@@ -2141,7 +2123,11 @@ hconv_mult_fn hconv_example_mult(int which) { return which == 0 ? example_mult_p
 // kernel description for a plan axis: threads per line group, groups per CTA, radix plan
 const char* hconv_plan_kernel(const hconv_plan* p, int axis) {
   if (!p || axis < 0 || axis >= (int)p->ax.size()) return "";
-  return p->ax[axis].k->radix;
+  const AxisPlan& ap = p->ax[axis];
+  // 1D plans whose unit-stride lines run the in-place two-residue kernel (launch_conv)
+  if (p->ax.size() == 1 && ap.ip_fn && !diag().no_ip && ap.dev.L <= ap.dev.B && ap.dev.n == hc::conv_ip_residues(ap.dev.Bc))
+    return "16x24x16 in place, two residues";
+  return ap.k->radix;
 }
 
 }  // extern "C"

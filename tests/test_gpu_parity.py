@@ -161,6 +161,25 @@ def test_conv1d_paired_kernel(cuda, oracle, L, M, m, C_):
     _check_conv(out[list(rows)], ref, f[list(rows)], g[list(rows)])
 
 
+@pytest.mark.parametrize("L,M,C_", [(6000, 11999, 300), (6144, 12288, 149), (6143, 12285, 151), (5000, 9000, 7),
+                                     (3100, 6200, 5), (100, 6150, 3), (6000, 11999, 1)])
+def test_conv1d_in_place_two_residue_kernel(cuda, oracle, L, M, C_):
+    """k_conv1d_ip4 (complex, m = 6144, n = 2: both residues of a line in flight, in-place passes,
+    buffers refilled by the last reader): more lines than CTAs, lines shorter than the block (masked
+    pass-0 loads and output stores), a single line, and the result overwriting the first input."""
+    rng = np.random.default_rng(L + C_)
+    f, g = _rand(rng, (C_, L)), _rand(rng, (C_, L))
+    plan = cuda.Conv1dPlan(L, M, 6144, cuda.Symmetry.Complex, C_=C_)
+    assert plan.params.n == 2 and "in place" in plan.kernel()
+    ft, gt = _t(f), _t(g)
+    out = cuda.convolve([ft, gt], plan.mult, plan, out=_t(f) * 0)[0].cpu().numpy()
+    rows = list(range(0, C_, max(1, C_ // 12)))
+    ref = np.stack([oracle.convolve([(L, M, 6144, 0)], f[c], g[c]) for c in rows])
+    _check_conv(out[rows], ref, f[rows], g[rows])
+    cuda.convolve([ft, gt], plan.mult, plan)  # in place
+    np.testing.assert_array_equal(ft.cpu().numpy(), out)
+
+
 def test_captured_convolution_replays(cuda):
     """CapturedConvolution (CUDA graph of the API call) gives the direct call's results, and a
     replay picks up new input values written into the same arrays."""

@@ -22,7 +22,9 @@ from paper_2303_17510_b200 import hconv  # noqa: E402
 
 # name: (kind, axes [(L, M, m, sym)], copies) -- the kernel each one selects
 CASES = {
-    "pp_c2": ("1d", [(6000, 11999, 6144, 0)], 301),       # persistent loop: > 2 lines per CTA        # k_conv1d_pp 16x16x24, TMEM stash + accumulator
+    "ip_c2": ("1d", [(6000, 11999, 6144, 0)], 301),       # k_conv1d_ip4: persistent loop (> 2 lines per CTA), both residues in flight
+    "ip_short": ("1d", [(3100, 9000, 6144, 0)], 449),     # k_conv1d_ip4, lines shorter than the block
+    "pp_c2": ("1d", [(6000, 11999, 6144, 0)], 301),       # k_conv1d_pp 16x16x24 (HCONV_NO_IP=1), TMEM stash + accumulator
     "pp2_4096": ("1d", [(4000, 7999, 4096, 0)], 301),      # k_conv1d_pp2 (paired forward FFTs)
     "pp_small": ("1d", [(1024, 2047, 1024, 0)], 2001),      # k_conv1d_pp, several CTAs per SM
     "pp_centered": ("1d", [(1023, 1534, 512, 1)], 3),    # centered ping-pong
@@ -36,7 +38,7 @@ CASES = {
 }
 
 
-ENV = {"single_stage_acc": {"HCONV_NO_PP": "1"}}
+ENV = {"single_stage_acc": {"HCONV_NO_PP": "1"}, "pp_c2": {"HCONV_NO_IP": "1"}}
 REPEAT = 3
 
 
