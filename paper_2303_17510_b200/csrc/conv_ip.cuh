@@ -89,7 +89,11 @@ __global__ void __launch_bounds__(Cfg::T, 1) k_conv1d_ip4(ConvArgs p) {
   static_assert(Cfg::P == 3, "three-pass plans");
   constexpr int T = Cfg::T, R0 = Cfg::R(0), R1 = Cfg::R(1), R2 = Cfg::R(2);
   constexpr int N = Cfg::N, N1 = R1 * R2, N2 = R2;
-  static_assert(T == 384 && R0 == 16 && R1 == 24 && R2 == 16, "12 warps; 4 groups: 2 pass-1 warps, 3 pass-2 warps");
+  // pass 1: R0 R2 butterflies on W1 warps, pass 2: R0 R1 butterflies on W2 warps; 4 groups of R0 / 4
+  // sub-sequences, each with W1 / 4 pass-1 warps and W2 / 4 pass-2 warps
+  constexpr int W1 = R0 * R2 / 32, W2 = R0 * R1 / 32, G1 = W1 / 4, G2 = W2 / 4;
+  static_assert(T == 384 && R0 == 16 && N1 == T && W1 % 4 == 0 && W2 % 4 == 0 && W1 <= 12 && W2 <= 12,
+                "12 warps; pass 0 on all of them; 4 groups");
   extern __shared__ __align__(16) double2 smem[];
   // TMA X, TMA Y, barrier X, barrier Y, then per buffer and group: pass 1 done, inverse pass 2 done
   __shared__ __align__(8) uint64_t bars[20];
@@ -111,21 +115,21 @@ __global__ void __launch_bounds__(Cfg::T, 1) k_conv1d_ip4(ConvArgs p) {
     mbar_init(&bars[2], T / 32);
     mbar_init(&bars[3], T / 32);
     for (int i = 0; i < 8; ++i) {
-      mbar_init(&bars[4 + i], 2);   // pass 1 done (2 warps): buffer i / 4, group i % 4
-      mbar_init(&bars[12 + i], 3);  // inverse pass 2 done (3 warps)
+      mbar_init(&bars[4 + i], G1);   // pass 1 done (G1 warps): buffer i / 4, group i % 4
+      mbar_init(&bars[12 + i], G2);  // inverse pass 2 done (G2 warps)
     }
     readers[0] = readers[1] = 0;
     fence_mbar_init();
   }
-  using TL = TmemLayout<T, 2 * R2, 0>;  // F of both residues
+  using TL = TmemLayout<32 * W2, 2 * R2, 0>;  // F of both residues, in the pass-2 warps' columns
   static_assert(TL::FITS, "both spectra in tensor memory");
   if (tid < 32) tmem_alloc(&tm_base, TL::COLS);
   tmem_fence_before();
   __syncthreads();
   tmem_fence_after();
-  // groups: as a pass-1 warp (warps 0..7) m1, as a pass-2 warp m2
-  const int m1 = (w >> 1) & 3, m2 = w / 3;
-  const bool w1 = w < 8;
+  // groups: as a pass-1 warp (warps 0..W1-1) m1, as a pass-2 warp (warps 0..W2-1) m2
+  const int m1 = (w / G1) & 3, m2 = (w / G2) & 3;
+  const bool w1 = w < W1, w2 = w < W2;
   const int base1 = N1 * (tid / N2), b1 = tid % N2;  // pass 1: sub-sequence offset and butterfly
   IpChain cA{X, 0, {smem_u32(&bars[2])}, {smem_u32(&bars[4 + m1])}, {smem_u32(&bars[4 + m2])},
              {smem_u32(&bars[12 + m2])}, {smem_u32(&bars[12 + m1])}, &bars[0], 0u, TL::f_addr(tm_base), &readers[0]};
@@ -197,6 +201,10 @@ __global__ void __launch_bounds__(Cfg::T, 1) k_conv1d_ip4(ConvArgs p) {
   const double2* gsrc = nullptr;   // the line's g (refill after pass 2 of f)
   const double2* fnext = nullptr;  // the next line's f (refill after inverse pass 0)
   auto fwd2f = [&](IpChain& c) HC_INL {
+    if (!w2) {
+      release(c, gsrc);
+      return;
+    }
     double2 v[R2];
     c.g1w.wait();
     sfor<R2>([&](auto Ai) HC_INL { v[Ai] = c.Z[base2 + (Ai ^ key2)]; });
@@ -205,11 +213,13 @@ __global__ void __launch_bounds__(Cfg::T, 1) k_conv1d_ip4(ConvArgs p) {
     tm_store<R2>(c.tf, v);
   };
   auto fwd2g = [&](IpChain& c) HC_INL {
+    if (!w2) return;
     double2 v[R2];
     c.g1w.wait();
     sfor<R2>([&](auto Ai) HC_INL { v[Ai] = c.Z[base2 + (Ai ^ key2)]; });
     DFT<R2, +1>::run(v);
     tmem_wait_st();
+    // (issuing these tensor-memory loads before the butterflies measured slower: 0.715 vs 0.701 ms)
     sfor<R2 / 4>([&](auto Ki) HC_INL {
       double2 F4[4];
       tm_ld4(c.tf + 16 * Ki, F4);

@@ -5,7 +5,16 @@
 namespace hc {
 
 // 16 x 24 x 16 at 12 warps: passes 0 and 2 (radix 16) on every warp, pass 1 (radix 24) on 8
+// (HC_IP_PLAN=2: 16 x 16 x 24, the radix-24 pass last and free of twiddles, on 8 warps with 24 values each:
+// spills at 168 registers, c2 0.70 -> 0.91 ms)
+#ifndef HC_IP_PLAN
+#define HC_IP_PLAN 1
+#endif
+#if HC_IP_PLAN == 2
+using CfgIp6144 = FFTCfg<Radices<16, 16, 24>, 384>;
+#else
 using CfgIp6144 = FFTCfg<Radices<16, 24, 16>, 384>;
+#endif
 
 const void* conv_ip_fn(int sym, int Bc) {
   if (sym == SYM_COMPLEX && Bc == 6144) return (const void*)k_conv1d_ip4<SYM_COMPLEX, CfgIp6144>;

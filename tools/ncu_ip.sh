@@ -1,5 +1,7 @@
 #!/bin/bash
-# one full ncu capture of the in-place c2 kernel (after a plain run); the report comes back in gpurun_out/
+# one full ncu capture of the in-place c2 kernel (after a plain run); the report comes back in
+# gpurun_out/ for per-instruction stall attribution here:
+#   ncu -i gpurun_out/ip_conv.ncu-rep --page source --csv --metrics smsp__pcsamp_warps_issue_stalled_long_scoreboard,...
 mkdir -p gpurun_out
 CMD="python tools/ab_conv.py 6000 11999 6144 4096"
 $CMD > gpurun_out/ip_plain.log 2>&1 || { echo plain failed; tail gpurun_out/ip_plain.log; exit 1; }
