@@ -203,6 +203,9 @@ inline void build_registry(KernelEntry* out, int* count) {
 #else
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
 #endif
+  // radix-7 plan: 3584 = 16 x 14 x 16 (the 7-smooth sizes of SPEC.md:523; DFT14 = 2 x 7 with the
+  // pair-form DFT7): blocks of 3584 complex / 7168 Hermitian points
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 14, 16>, 256>, 1>("16x14x16");
   // radix-5 plan: 6000 = 10 x 24 x 25 (the 5-smooth sizes of SPEC.md:523's search space, e.g.
   // c2's m = 6000 = L, p = 1, q = 2)
   out[k++] = make_entry<SYM, FFTCfg<Radices<10, 24, 25>, 320>, 1>("10x24x25");

@@ -45,7 +45,7 @@ def test_fill_uniform_matches_oracle(cuda, oracle):
 
 
 # -------------------------------------------------------------- residue level ----
-FAST_BC = [64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 4096, 6000, 6144]
+FAST_BC = [64, 128, 256, 384, 512, 768, 1024, 1536, 2048, 3072, 3584, 4096, 6000, 6144]
 
 
 def _residue_cases():
