@@ -185,6 +185,12 @@ KernelEntry make_naive_entry() {
 template <int SYM>
 inline void build_registry(KernelEntry* out, int* count) {
   int k = 0;
+#ifdef HC_REGISTRY_MIN
+  // development builds (make VARIANT=dev EXTRA=-DHC_REGISTRY_MIN): the 4096-point plan only
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
+  out[k++] = make_naive_entry<SYM>();
+  *count = k;
+#else
   out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4, false, 4>("8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4, false, 4>("16x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
@@ -211,6 +217,7 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<10, 24, 25>, 320>, 1>("10x24x25");
   out[k++] = make_naive_entry<SYM>();
   *count = k;
+#endif
 }
 
 }  // namespace hc
