@@ -180,6 +180,24 @@ def test_conv1d_in_place_two_residue_kernel(cuda, oracle, L, M, C_):
     np.testing.assert_array_equal(ft.cpu().numpy(), out)
 
 
+def test_conv1d_in_place_kernel_random_shapes(cuda, oracle):
+    """k_conv1d_ip4 over random (L, M, copies) within its domain (L <= 6144 < M <= 12288), every row
+    against the oracle; the planner's c2 plan runs this kernel."""
+    rng = np.random.default_rng(20230317)
+    for _ in range(8):
+        L = int(rng.integers(1, 6145))
+        M = int(rng.integers(6145, 12289))
+        C_ = int(rng.integers(1, 12))
+        f, g = _rand(rng, (C_, L)), _rand(rng, (C_, L))
+        plan = cuda.Conv1dPlan(L, M, 6144, cuda.Symmetry.Complex, C_=C_)
+        assert "in place" in plan.kernel()
+        out = cuda.convolve([_t(f), _t(g)], plan.mult, plan, out=_t(f) * 0)[0].cpu().numpy()
+        ref = np.stack([oracle.convolve([(L, M, 6144, 0)], f[c], g[c]) for c in range(C_)])
+        _check_conv(out, ref, f, g)
+    plan = cuda.Conv1dPlan(6000, 11999, None, cuda.Symmetry.Complex, C_=4096)  # planner
+    assert plan.params.m == 6144 and "in place" in plan.kernel()
+
+
 def test_captured_convolution_replays(cuda):
     """CapturedConvolution (CUDA graph of the API call) gives the direct call's results, and a
     replay picks up new input values written into the same arrays."""
