@@ -54,6 +54,7 @@ constexpr int column_groups() {
 }
 
 // pipelined column tiles: two tile buffers per CTA, so up to half the groups of column_groups
+// (4 columns per tile -- 64-byte rows, two CTAs per SM -- measured slower: c5 9.91 -> 12.42 ms)
 template <class Cfg>
 constexpr int column_groups_pp() {
   int g = 8;
@@ -186,7 +187,9 @@ template <int SYM>
 inline void build_registry(KernelEntry* out, int* count) {
   int k = 0;
 #ifdef HC_REGISTRY_MIN
-  // development builds (make VARIANT=dev EXTRA=-DHC_REGISTRY_MIN): the 4096-point plan only
+  // development builds (make VARIANT=dev EXTRA=-DHC_REGISTRY_MIN): the plans of c3 / c4 / c5 only
+  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
   out[k++] = make_naive_entry<SYM>();
   *count = k;
