@@ -661,7 +661,9 @@ def main():
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "cuda":
         sys.exit(self_launch(args))
     if args.launch_check:  # test hook: the rank layout bench.py runs with (no GPU work)
-        print(json.dumps({"rank": rank, "world": world, "local": local, "config": default_config(args)}), flush=True)
+        line = json.dumps({"rank": rank, "world": world, "local": local, "config": default_config(args)}) + "\n"
+        sys.stdout.flush()
+        os.write(1, line.encode())  # one write per rank: the ranks share the launcher's pipe
         return
     if args.impl == "reference":
         run_reference(args)

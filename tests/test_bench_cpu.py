@@ -17,7 +17,15 @@ def test_self_launch_spawns_one_rank_per_gpu():
     out = subprocess.run([sys.executable, str(REPO / "bench.py"), "--gpus", "2", "--launch-check"],
                          capture_output=True, text=True, timeout=300, cwd=REPO)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    lines = []
+    for l in out.stdout.splitlines():  # the launcher may add lines of its own
+        if l.startswith("{"):
+            try:
+                d = json.loads(l)
+            except ValueError:
+                continue
+            if isinstance(d, dict) and "rank" in d:
+                lines.append(d)
     assert sorted(l["rank"] for l in lines) == [0, 1]
     assert all(l["world"] == 2 for l in lines)
     assert sorted(l["local"] for l in lines) == [0, 1]
