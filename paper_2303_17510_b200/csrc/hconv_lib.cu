@@ -69,7 +69,7 @@ struct NcclError : std::runtime_error {
 // Diagnostics switches, read once from the environment (HCONV_*; tools/README.md).  None of
 // them is needed in production: the defaults are the measured-best choices.
 struct Diag {
-  bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, no_cols_tma, sync_mult;
+  bool poison, no_stage, no_pp, pp2, same_line, no_tmacc, trace, no_cols, no_cols_pp, no_cols_tma, no_cols_tma1, sync_mult;
   bool no_ip;       // HCONV_NO_IP=1: never the in-place two-residue kernel (conv_ip.cuh)
   bool fake_timer;  // planner test hook: every candidate times 1 ms
   int dbg;
@@ -89,6 +89,7 @@ struct Diag {
     no_cols = on("HCONV_NO_COLS");
     no_cols_pp = on("HCONV_NO_COLS_PP");
     no_cols_tma = on("HCONV_NO_COLS_TMA");
+    no_cols_tma1 = on("HCONV_NO_COLS_TMA1");
     sync_mult = on("HCONV_SYNC_MULT");
     fake_timer = on("HCONV_PLAN_FAKE_TIMER");
     dbg = (int)num("HCONV_DBG", 0);
@@ -631,6 +632,40 @@ int cols_tma_tabn(const AxisPlan& ap, int rows_in, int box_in, int rows_out, int
   return tabn;
 }
 int box_rows_for(int rows) { return rows >= 256 ? 256 : ((rows + 7) / 8) * 8; }
+// smem of the one-buffer TMA column kernels (k_pfft_*_cols_tma1, gc columns per tile): tables, the
+// 128-byte-aligned exchange / block buffer X of *bufn values and, for the forward pass, the input
+// staging area of the data rows behind it; 0 = does not fit or not instantiated
+int cols_tma1_tabn(const AxisPlan& ap, bool fwd, int rows_in, int box_in, int rows_out, int box_out, size_t* smem,
+                   int* bufn, int* nb_stage = nullptr) {
+  if (diag().no_cols_tma || diag().no_cols_tma1 || !ap.k->fwdc1) return 0;
+  const int rin = (rows_in + box_in - 1) / box_in * box_in, rout = (rows_out + box_out - 1) / box_out * box_out;
+  const size_t gc = (size_t)ap.k->gc, cap = kSmemCap / sizeof(double2);
+  const size_t x = (gc * (size_t)std::max({ap.k->xs, rout, fwd ? 0 : rin}) + 7) & ~(size_t)7;
+  size_t in = fwd ? (gc * (size_t)rin + 7) & ~(size_t)7 : 0;
+  if (x + in + (size_t)ap.k->mt + 8 > cap) return 0;
+  if (!fwd) {
+    // inverse: stage as many leading boxes as fit next to X and every table (at least one box
+    // stays for the late load into X, so both barriers complete every tile)
+    const size_t tabs = std::max<size_t>((size_t)ap.k->mt, (size_t)ap.tab_full);
+    const size_t box = gc * (size_t)box_in;
+    const size_t room = cap > x + tabs + 8 ? cap - x - tabs - 8 : 0;
+    const size_t nb = std::min<size_t>(room / box, (size_t)(rin / box_in) - 1);
+    in = nb * box;
+    if (nb_stage) *nb_stage = (int)nb;
+  }
+  const size_t room = cap - x - in - 8;
+  const int tabn = (int)std::max<size_t>((size_t)ap.k->mt, std::min<size_t>((size_t)ap.tab_full, room));
+  *smem = ((size_t)tabn + 8 + x + in) * sizeof(double2);  // + 128 B: the kernel aligns the buffers
+  *bufn = (int)x;
+  return tabn;
+}
+int stage_boxes_limit() {  // HCONV_TMA1_STAGE=k caps the staged boxes of the inverse (diagnostics)
+  static const int v = [] {
+    const char* e = std::getenv("HCONV_TMA1_STAGE");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
 
 void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout, const double2* f, void* F, int v,
                 int ref_order, cudaStream_t s) {
@@ -648,6 +683,24 @@ void launch_fwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
       a.ax.tabn = tt;
       const hc::TileMaps tm{(int)lin.nin, rows, bi, bo, bufn};
       ap.k->fwdct(a, tm, mi, mo, grid, smt, s);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
+  if (use_cols(ap, lin) && !ref_order) {
+    // blocks without room for two full-width tile buffers: one buffer plus the staged data rows
+    const int rows = (int)ap.data, bi = box_rows_for(rows), bo = box_rows_for(ap.dev.Bc);
+    size_t smt = 0;
+    int bufn = 0;
+    const int tt = cols_tma1_tabn(ap, true, rows, bi, ap.dev.Bc, bo, &smt, &bufn);
+    CUtensorMap mi, mo;
+    if (tt > 0 && lin.count % ap.k->gc == 0 && lout.count % ap.k->gc == 0 && lout.nin == lin.nin &&
+        tile_map(&mi, f, lin, rows, ap.k->gc, bi) && tile_map(&mo, F, lout, ap.dev.Bc, ap.k->gc, bo)) {
+      const int grid = grid_cols(ap.k->fwdc1_fn, ap.k, smt, lin.count, ap.k->gc);
+      hc::FwdArgs a{ap.dev, lin, lout, f, F, v, ref_order};
+      a.ax.tabn = tt;
+      const hc::TileMaps tm{(int)lin.nin, rows, bi, bo, bufn};
+      ap.k->fwdc1(a, tm, mi, mo, grid, smt, s);
       CK(cudaGetLastError());
       return;
     }
@@ -696,6 +749,27 @@ void launch_bwd(const AxisPlan& ap, const hc::Lines& lin, const hc::Lines& lout,
       a.ax.tabn = tt;
       const hc::TileMaps tm{(int)lin.nin, rows, bi, bi, bufn};
       ap.k->bwdct(a, tm, mi, grid, smt, s);
+      CK(cudaGetLastError());
+      return;
+    }
+  }
+  if (use_cols(ap, lout) && !ref_order) {
+    const int rows = ap.dev.Bc, bi = box_rows_for(rows);
+    size_t smt = 0;
+    int bufn = 0;
+    int nbs = 0;
+    int tt = cols_tma1_tabn(ap, false, rows, bi, rows, bi, &smt, &bufn, &nbs);
+    if (tt > 0 && stage_boxes_limit() >= 0 && stage_boxes_limit() < nbs) {
+      smt -= (size_t)(nbs - stage_boxes_limit()) * ap.k->gc * bi * sizeof(double2);
+      nbs = stage_boxes_limit();
+    }
+    CUtensorMap mi;
+    if (tt > 0 && lin.count % ap.k->gc == 0 && lout.count % ap.k->gc == 0 && tile_map(&mi, F, lin, rows, ap.k->gc, bi)) {
+      const int grid = grid_cols(ap.k->bwdc1_fn, ap.k, smt, lin.count, ap.k->gc);
+      hc::BwdArgs a{ap.dev, lin, lout, F, dst, acc, scale, v, ref_order};
+      a.ax.tabn = tt;
+      const hc::TileMaps tm{(int)lin.nin, rows, bi, bi, bufn, nbs};
+      ap.k->bwdc1(a, tm, mi, grid, smt, s);
       CK(cudaGetLastError());
       return;
     }

@@ -1366,6 +1366,7 @@ struct TileMaps {
   int rows_in;         // rows of the input tile (data rows, or the block for the inverse)
   int box_in, box_out; // rows per tensor box (<= 256) of the input and output maps
   int bufn;            // complex values per tile buffer (host: >= every box row written or read)
+  int nb_stage = 0;    // k_pfft_bwd_cols_tma1: leading input boxes prefetched into the staging area
 };
 template <int SYM, class Cfg, int GC>
 __global__ void __launch_bounds__(Cfg::T * GC, 1)
@@ -1503,6 +1504,199 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
     store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
     __syncthreads();  // X (this tile's exchanges) is free before the next issue into it
+  }
+}
+
+// Whole-CTA barriers whose first write-after-read wait (before the first exchange's stores) runs a
+// gate instead: used when the exchange buffer is released by something other than this transform.
+template <class Gate>
+struct GatedCtaSync {
+  const Gate& gate;
+  mutable bool open = false;
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+  __device__ __forceinline__ void war_arrive() const { __syncthreads(); }
+  __device__ __forceinline__ void war_wait() const {
+    if (!open) gate();
+    open = true;
+  }
+};
+#ifndef HC_TMA1_FWD
+#define HC_TMA1_FWD 1
+#endif
+// ------------------------------- column-tile pfft, tensor-map TMA, one tile buffer --
+// Blocks too long for two tile buffers at the full tile width (c4's 4096-point columns: one
+// buffer of 2 columns is 139 KB) still overlap their copies with the butterflies:
+//  * forward: the raw tile is only the data rows (half a block or less for explicit padding), so
+//    it is prefetched by TMA into a separate staging area IN behind the exchange buffer X while
+//    the previous tile transforms; the finished block leaves X by tensor stores, whose
+//    shared-memory reads are waited for just before the next tile's first exchange;
+//  * inverse: the leading boxes of the next block tile (as many as fit behind X) are prefetched
+//    into a staging area while the current tile transforms; the rest is loaded into X itself as
+//    soon as the last exchange of the current tile has been read (fft_inverse's hook), i.e. behind
+//    the pass-0 butterflies, the post-twiddles and the strided output stores.
+// Same tiles, maps and arithmetic as the two-buffer kernels above (bit-identical results).
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1)
+    k_pfft_fwd_cols_tma1(FwdArgs p, TileMaps tm, const __grid_constant__ CUtensorMap min,
+                         const __grid_constant__ CUtensorMap mout) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bar;
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  constexpr int N = Cfg::N;
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  const int rows = tm.rows_in;
+  double2* X = align_smem128(smem + a.tabn);
+  double2* IN = X + tm.bufn;  // bufn is a multiple of 8 values: IN stays 128-byte aligned
+  const long long ntiles = p.lin.count / GC;
+  const bool leader = threadIdx.x == 0;
+  const int kBox = tm.box_in;
+  const int nbox_in = (rows + kBox - 1) / kBox;
+  const uint32_t box_bytes = (uint32_t)GC * 16u * (uint32_t)kBox;
+  auto issue = [&](long long t) HC_INL {
+    if (t >= ntiles) return;
+    const long long item = t * GC;
+    const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+    mbar_expect_tx(&bar, box_bytes * (uint32_t)nbox_in);
+    for (int r = 0; r < nbox_in; ++r) tma_tensor_load_3d(IN + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bar);
+  };
+  if (leader) {
+    tma_prefetch_map(&min);
+    tma_prefetch_map(&mout);
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (leader) issue(blockIdx.x);
+  uint32_t ph = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    mbar_wait(&bar, ph);
+    ph ^= 1;
+    double2 v[Cfg::E];
+    load_pass0<SYM, Cfg>(v, a, tp, IN + g, GC, p.v, tid);
+#if HC_TMA1_FWD == 0
+    if (leader) bulk_wait_read();  // the previous tile's tensor stores have read X
+    __syncthreads();               // IN is consumed, X is free
+    if (leader) issue(t + gridDim.x);
+    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+#else
+    // one barrier behind the pass-0 butterflies says both "IN is consumed" (the next tile's copy
+    // may start) and "X is free" (the previous tile's tensor stores have read it)
+    auto gate = [&]() HC_INL {
+#if HC_TMA1_FWD == 1
+      if (leader) bulk_wait_read();
+#endif
+      __syncthreads();
+      if (leader) issue(t + gridDim.x);
+    };
+    const GatedCtaSync<decltype(gate)> gs{gate};
+    fft_forward<Cfg, GatedCtaSync<decltype(gate)>, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, gs, p0);
+#endif
+#if HC_TMA1_FWD == 2
+    // the block leaves from registers (coalesced GC-column runs), nothing waits for X
+    const long long ob = p.lout.base(t * GC + g), oes = p.lout.es;
+    double2* F = (double2*)p.F;
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { F[ob + (beta + (long long)RpL * Ki) * oes] = v[c * RL + Ki]; });
+    });
+#else
+    __syncthreads();  // the last exchange's reads are done: X takes the block [k][GC]
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL { X[(beta + RpL * Ki) * GC + g] = v[c * RL + Ki]; });
+    });
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (leader) {
+      const long long item = t * GC;
+      const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+      for (int r = 0; r * tm.box_out < N; ++r)
+        tma_tensor_store_3d(&mout, c0, r * tm.box_out, c2, X + (size_t)r * tm.box_out * GC);
+      bulk_commit();
+    }
+#endif
+  }
+  if (leader) bulk_wait_all();
+}
+
+template <int SYM, class Cfg, int GC>
+__global__ void __launch_bounds__(Cfg::T * GC, 1)
+    k_pfft_bwd_cols_tma1(BwdArgs p, TileMaps tm, const __grid_constant__ CUtensorMap min) {
+  static_assert(SYM != SYM_HERMITIAN, "column tiles serve outer (non-Hermitian) axes");
+  extern __shared__ __align__(16) double2 smem[];
+  __shared__ __align__(8) uint64_t bars[2];  // 0: the staged leading boxes (S), 1: the boxes loaded into X
+  constexpr int T = Cfg::T, RL = Cfg::R(Cfg::P - 1), CL = Cfg::C(Cfg::P - 1), RpL = Cfg::Rprod(Cfg::P - 1);
+  constexpr int N = Cfg::N;
+  const int g = threadIdx.x % GC, tid = threadIdx.x / GC;
+  const AxisDev& a = p.ax;
+  double2* tb = smem;
+  const double2* mt = tb;
+  stage_tables(tb, a, a.tabn);
+  const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
+  const P0Res<SYM> p0{&a, tp, p.v};
+  double2* X = align_smem128(smem + a.tabn);
+  double2* S = X + tm.bufn;  // the first nb_stage boxes of the next tile wait here
+  const long long ntiles = p.lin.count / GC;
+  const bool leader = threadIdx.x == 0;
+  const int kBox = tm.box_in;
+  const int nbox = (N + kBox - 1) / kBox, nbs = tm.nb_stage;
+  const int rows_s = nbs * kBox;  // block rows below this are read from S
+  const uint32_t box_bytes = (uint32_t)GC * 16u * (uint32_t)kBox;
+  auto issue = [&](long long t, int r0, int r1, double2* dst, uint64_t* bar) HC_INL {
+    if (t >= ntiles || r0 >= r1) return;
+    const long long item = t * GC;
+    const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
+    mbar_expect_tx(bar, box_bytes * (uint32_t)(r1 - r0));
+    for (int r = r0; r < r1; ++r) tma_tensor_load_3d(dst + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, bar);
+  };
+  if (leader) {
+    tma_prefetch_map(&min);
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (leader) {
+    issue(blockIdx.x, 0, nbs, S, &bars[0]);
+    issue(blockIdx.x, nbs, nbox, X, &bars[1]);
+  }
+  uint32_t ph = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    if (nbs > 0) mbar_wait(&bars[0], ph);
+    if (nbs < nbox) mbar_wait(&bars[1], ph);
+    ph ^= 1;
+    double2 v[Cfg::E];
+    sfor<CL>([&](auto Ci) HC_INL {
+      constexpr int c = Ci;
+      const int beta = tid + c * T;
+      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
+        sfor<RL>([&](auto Ki) HC_INL {
+          const int row = beta + RpL * Ki;
+          v[c * RL + Ki] = (row < rows_s ? S : X)[row * GC + g];
+        });
+    });
+    __syncthreads();  // the block is in registers: S may be refilled, the exchanges may use X
+    if (leader) issue(t + gridDim.x, 0, nbs, S, &bars[0]);
+    // the rest of the next block goes into X itself behind the barrier that ends the last exchange
+    // (fft_inverse's hook), i.e. behind the pass-0 butterflies and the strided output stores
+    auto next = [&]() HC_INL {
+      if (leader) issue(t + gridDim.x, nbs, nbox, X, &bars[1]);
+    };
+    fft_inverse<Cfg, CtaSync, P0Res<SYM>, decltype(next), GC>(v, X + g, mt, tid, CtaSync(), p0, next);
+    const long long ob = p.lout.base(t * GC + g);
+    const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
+    store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
   }
 }
 

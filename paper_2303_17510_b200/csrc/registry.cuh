@@ -42,6 +42,13 @@ struct KernelEntry {
   void (*fwdct)(const FwdArgs&, const TileMaps&, const CUtensorMap&, const CUtensorMap&, int grid, size_t smem,
                 cudaStream_t) = nullptr;
   void (*bwdct)(const BwdArgs&, const TileMaps&, const CUtensorMap&, int grid, size_t smem, cudaStream_t) = nullptr;
+  // one-buffer TMA tiles at the full width gc (k_pfft_*_cols_tma1), for blocks whose two-buffer
+  // tiles would be narrower (gcp < gc)
+  const void* fwdc1_fn = nullptr;
+  const void* bwdc1_fn = nullptr;
+  void (*fwdc1)(const FwdArgs&, const TileMaps&, const CUtensorMap&, const CUtensorMap&, int grid, size_t smem,
+                cudaStream_t) = nullptr;
+  void (*bwdc1)(const BwdArgs&, const TileMaps&, const CUtensorMap&, int grid, size_t smem, cudaStream_t) = nullptr;
 };
 
 // column groups per CTA: up to 8 adjacent columns (128 B rows), <= 1024 threads, and the
@@ -134,6 +141,19 @@ KernelEntry make_entry(const char* radix) {
     e.bwdct = [](const BwdArgs& a, const TileMaps& tm, const CUtensorMap& mi, int grid, size_t sm, cudaStream_t s) {
       k_pfft_bwd_cols_tma<SYM, Cfg, GP><<<grid, Cfg::T * GP, sm, s>>>(a, tm, mi);
     };
+    // (plans of more than 16 values per thread run GC x T > 512 threads at capped registers: their
+    // tiles stay with the plain-load kernels)
+    if constexpr (GP < GC && Cfg::E <= 16) {
+      e.fwdc1_fn = (const void*)k_pfft_fwd_cols_tma1<SYM, Cfg, GC>;
+      e.bwdc1_fn = (const void*)k_pfft_bwd_cols_tma1<SYM, Cfg, GC>;
+      e.fwdc1 = [](const FwdArgs& a, const TileMaps& tm, const CUtensorMap& mi, const CUtensorMap& mo, int grid,
+                   size_t sm, cudaStream_t s) {
+        k_pfft_fwd_cols_tma1<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a, tm, mi, mo);
+      };
+      e.bwdc1 = [](const BwdArgs& a, const TileMaps& tm, const CUtensorMap& mi, int grid, size_t sm, cudaStream_t s) {
+        k_pfft_bwd_cols_tma1<SYM, Cfg, GC><<<grid, Cfg::T * GC, sm, s>>>(a, tm, mi);
+      };
+    }
   }
   return e;
 }

@@ -28,10 +28,11 @@ def test_stress_case(cuda, case):
     assert "bit-identical" in r.stdout
 
 
-@pytest.mark.parametrize("case", ["cols_2d", "cols_3d_herm", "cols_3d_c5_like"])
+@pytest.mark.parametrize("case", ["cols_2d", "cols_3d_herm", "cols_3d_c5_like", "cols_2d_4096", "cols_2d_2048"])
 def test_tma_column_tiles_bit_identical(cuda, case, tmp_path):
-    """The tensor-map TMA column kernels move the same tiles as the cp.async kernels: identical
-    arithmetic, so identical bits (HCONV_NO_COLS_TMA=1 selects the cp.async path)."""
+    """The tensor-map TMA column kernels (two tile buffers, or one buffer plus staged rows for the
+    long blocks) move the same tiles as the cp.async / plain-load kernels: identical arithmetic, so
+    identical bits (HCONV_NO_COLS_TMA=1 selects the non-TMA path)."""
     outs = []
     for flag in ("0", "1"):
         env = dict(os.environ, HCONV_NO_COLS_TMA=flag)

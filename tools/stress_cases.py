@@ -34,6 +34,9 @@ CASES = {
     "cols_2d": ("nd", [(256, 511, 256, 0), (192, 383, 128, 0)], 1),   # column tiles + inner conv
     "cols_3d_herm": ("nd", [(31, 46, 16, 1), (31, 46, 16, 1), (31, 46, 16, 2)], 1),
     "cols_3d_c5_like": ("nd", [(511, 766, 768, 1), (511, 766, 768, 1), (15, 22, 32, 2)], 1),  # c5 x/y tiles
+    # one-buffer TMA column tiles (k_pfft_*_cols_tma1): blocks too long for two tile buffers, more tiles than CTAs
+    "cols_2d_4096": ("nd", [(2048, 4095, 4096, 0), (320, 639, 128, 0)], 1),          # c4's x tiles: 2 columns of 4096 points
+    "cols_2d_2048": ("nd", [(2047, 3070, 1024, 1), (1279, 1918, 1024, 2)], 1),        # centered, 3 residues, 4 columns of 2048 points
     "general_op": ("gen", [(1000, 1999, 1024, 0)], 3),   # conv1d_general (A = 3 product)
 }
 
