@@ -1425,7 +1425,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     load_pass0<SYM, Cfg>(v, a, tp, X + g, GC, p.v, tid);
     __syncthreads();  // the staged tile is consumed before the first exchange overwrites it
     fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
-    __syncthreads();  // the last exchange's reads are done: X takes the block [k][GC]
+    // (fft_forward ends its last exchange with a CTA barrier: every read of X is done, X takes the block [k][GC])
     sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;
@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     const long long ob = p.lout.base(t * GC + g);
     const Emit em{p.dst + ob, p.lout.es, p.acc ? p.acc + ob : nullptr, p.lout.es, p.scale};
     store_pass0<SYM, Cfg>(v, a, tp, em, p.v, tid);
-    __syncthreads();  // X (this tile's exchanges) is free before the next issue into it
+    // (X is free for the next issue into it: fft_inverse ends its last exchange with a CTA barrier)
   }
 }
 
@@ -1609,7 +1609,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
         sfor<RL>([&](auto Ki) HC_INL { F[ob + (beta + (long long)RpL * Ki) * oes] = v[c * RL + Ki]; });
     });
 #else
-    __syncthreads();  // the last exchange's reads are done: X takes the block [k][GC]
+    // (fft_forward ends its last exchange with a CTA barrier: every read of X is done, X takes the block [k][GC])
     sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
       const int beta = tid + c * T;

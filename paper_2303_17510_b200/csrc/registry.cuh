@@ -211,6 +211,9 @@ inline void build_registry(KernelEntry* out, int* count) {
   out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
   out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
+#ifdef HC_REGISTRY_C2  // + c2's 6144-point plan (the in-place kernel's host plumbing hangs off it)
+  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
+#endif
   out[k++] = make_naive_entry<SYM>();
   *count = k;
 #else

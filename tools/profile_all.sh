@@ -2,7 +2,7 @@
 # launch lists of the non-headline configurations (fixed plans: no planner launches); each ncu pass
 # only after the same command exited 0 without ncu.  Usage: bash tools/profile_all.sh [c1 c3 c4 c5]
 mkdir -p gpurun_out
-declare -A M=([c1]=2048 [c3]=8192 [c4]=4096,2048 [c5]=768,768,1024)
+declare -A M=([c1]=2048 [c3]=8192 [c4]=4096,4096 [c5]=768,768,1024)
 for c in ${@:-c1 c3 c4 c5}; do
   CMD="python bench.py --config $c --m ${M[$c]} --steps 1 --warmup 3 --no-cpu --single"
   $CMD > gpurun_out/plain_$c.json 2> gpurun_out/plain_$c.err || { echo "$c plain failed"; tail -3 gpurun_out/plain_$c.err; continue; }
