@@ -538,6 +538,22 @@ def run_cuda(args):
     name = default_config(args)
     dims = CONFIGS[name][0]
     t1 = None
+    watchdog = None
+    if world > 1:
+        # a collective that never completes (a lost rank, a wedged link) must not hang the driver: after
+        # HCONV_BENCH_TIMEOUT seconds rank 0 prints an error line and every rank exits non-zero
+        import threading
+
+        def bail():
+            if rank == 0:
+                print(json.dumps({"metric": "complex128 dealiased-convolution output points/s", "value": None,
+                                  "n_gpus": world, "error": "multi-GPU run timed out", "config": config_dict(name, world)}),
+                      flush=True)
+            os._exit(3)
+
+        watchdog = threading.Timer(float(os.environ.get("HCONV_BENCH_TIMEOUT", "1500")), bail)
+        watchdog.daemon = True
+        watchdog.start()
     if world > 1 and dims > 1 and not args.no_t1:
         # T_1: the same global problem on one GPU (rank 0 alone, the single-device path)
         if rank == 0:
@@ -578,6 +594,8 @@ def run_cuda(args):
                     others[o]["exchange"] = r["exchange"]
             except Exception as e:  # noqa: BLE001 -- a side config must not lose the headline line
                 others[o] = {"error": repr(e)[:300]}
+    if watchdog is not None:
+        watchdog.cancel()
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
