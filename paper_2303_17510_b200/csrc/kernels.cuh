@@ -180,6 +180,48 @@ __device__ __forceinline__ void herm_pack(double2* X, const AxisDev& a, const do
   }
 }
 
+// Heavily padded Hermitian lines (S <= Bc/2, herm_pack's fast path) straight into pass-0 layout:
+// element j = Ns1 a + b of Z' depends on one stored value only (k = j below Bc/2, k = Bc - j
+// above: W_{Bc-k} = 0), so the packed line never takes the round trip through shared memory
+// (herm_pack writes 2 values per quad, load_plain reads them back) and one barrier goes away; the
+// low factor of zeta_B^k is the same for a thread's lower (kl = b) and upper (kl = -b mod Ns1)
+// elements and is read once each.  Same values as herm_pack + load_plain (each Z'_j is formed by
+// the same operations on the same operands).
+template <class Cfg>
+__device__ __forceinline__ void herm_load_padded(double2 (&v)[Cfg::E], const double2* X, const AxisDev& a,
+                                                 const double2* tb, int res, int tid) {
+  constexpr int R0 = Cfg::R(0), C0 = Cfg::C(0), Ns1 = Cfg::Ns(1), Bc = Cfg::N, half = Bc / 2;
+  const int S = a.S;
+  const double2* Zr = tb + (a.oZ + res * Ns1);
+  const double2* Ur = tb + (a.oU + res * a.nu);
+  const double2* Bl = tb + a.oBl;
+  const double2* Bh = tb + a.oBh;
+  sfor<C0>([&](auto Ci) HC_INL {
+    constexpr int c = Ci;
+    const int b = tid + c * Cfg::T;
+    if (bvalid<Cfg, 0>(c, tid)) {
+      const int bu = (Ns1 - b) % Ns1;  // kl of the upper elements
+      const double2 blo = Bl[b], bup = Bl[bu];
+      double2 zlo = make_double2(1.0, 0.0), zup = zlo;
+      if (res) {
+        zlo = Zr[b];
+        zup = Zr[bu];
+      }
+      sfor<R0>([&](auto Ai) HC_INL {
+        constexpr int ai = Ai;
+        const int j = Ns1 * ai + b;
+        const bool low = j <= half;
+        const int k = low ? j : Bc - j;
+        const int kh = k / Ns1;
+        double2 wk = k < S ? X[k] : make_double2(0.0, 0.0);
+        if (res) wk = cmul(wk, cmul(low ? zlo : zup, Ur[kh]));  // zeta_qm^{v k}
+        const double2 o = cmul(wk, cmul(Bh[kh], low ? blo : bup));
+        v[c * R0 + ai] = low ? make_double2(wk.x - o.y, wk.y + o.x) : make_double2(wk.x + o.y, o.x - wk.y);
+      });
+    }
+  });
+}
+
 // pass-0 values straight from a shared-memory line in natural order (v[c R0 + a] = X[Ns1 a + b])
 template <class Cfg>
 __device__ __forceinline__ void load_plain(double2 (&v)[Cfg::E], const double2* X, int tid) {
@@ -721,9 +763,13 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) {
-          herm_pack<T, Cfg::Ns(1)>(X, a, tb, res, tid);
-          sync();
-          load_plain<Cfg>(v, X, tid);
+          if (a.S <= Cfg::N / 2) {
+            herm_load_padded<Cfg>(v, X, a, tb, res, tid);
+          } else {
+            herm_pack<T, Cfg::Ns(1)>(X, a, tb, res, tid);
+            sync();
+            load_plain<Cfg>(v, X, tid);
+          }
         } else {
           load_pass0_pp<SYM, Cfg>(v, a, tb, X, res, tid);
         }
@@ -759,9 +805,13 @@ __global__ void __launch_bounds__(Cfg::T * G, MINB) k_conv1d_pp(ConvArgs p) {
       HC_TRACE();
       if (!(p.dbg & 2)) {
         if constexpr (SYM == SYM_HERMITIAN) {
-          herm_pack<T, Cfg::Ns(1)>(Y, a, tb, res, tid);
-          sync();
-          load_plain<Cfg>(v, Y, tid);
+          if (a.S <= Cfg::N / 2) {
+            herm_load_padded<Cfg>(v, Y, a, tb, res, tid);
+          } else {
+            herm_pack<T, Cfg::Ns(1)>(Y, a, tb, res, tid);
+            sync();
+            load_plain<Cfg>(v, Y, tid);
+          }
         } else {
           load_pass0_pp<SYM, Cfg>(v, a, tb, Y, res, tid);
         }
@@ -1349,6 +1399,19 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols_pp(BwdArgs p) 
   cp_async_wait<0>();
 }
 
+// Whole-CTA barriers whose first write-after-read wait (before the first exchange's stores) runs a
+// gate instead: used when the exchange buffer is released by something other than this transform.
+template <class Gate>
+struct GatedCtaSync {
+  const Gate& gate;
+  mutable bool open = false;
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+  __device__ __forceinline__ void war_arrive() const { __syncthreads(); }
+  __device__ __forceinline__ void war_wait() const {
+    if (!open) gate();
+    open = true;
+  }
+};
 // ------------------------------------------ column-tile pfft, tensor-map TMA --
 // The pipelined column tiles with every tile moved by the TMA engine instead of per-thread
 // copies: a 3D tensor map {inner columns, rows, outer} (float64 pairs) describes the strided
@@ -1415,16 +1478,23 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int b = k & 1;
     double2* X = buf[b];
-    if (leader) {
-      bulk_wait_read();  // the other buffer's last tensor store has read its block
-      issue(t + gridDim.x, b ^ 1);
-    }
     mbar_wait(&bars[b], ph[b]);
     ph[b] ^= 1;
     double2 v[Cfg::E];
     load_pass0<SYM, Cfg>(v, a, tp, X + g, GC, p.v, tid);
-    __syncthreads();  // the staged tile is consumed before the first exchange overwrites it
-    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
+    // behind the pass-0 butterflies: the next tile's copy into the other buffer, once that buffer's
+    // last tensor store has read its block (waiting for it at the top of the tile stalled the
+    // leader, and with it the CTA, for the store's whole shared-memory read), and the barrier that
+    // says the staged tile is consumed before the first exchange overwrites it
+    auto gate = [&]() HC_INL {
+      if (leader) {
+        bulk_wait_read();
+        issue(t + gridDim.x, b ^ 1);
+      }
+      __syncthreads();
+    };
+    const GatedCtaSync<decltype(gate)> gs{gate};
+    fft_forward<Cfg, GatedCtaSync<decltype(gate)>, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, gs, p0);
     // (fft_forward ends its last exchange with a CTA barrier: every read of X is done, X takes the block [k][GC])
     sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
@@ -1507,22 +1577,6 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   }
 }
 
-// Whole-CTA barriers whose first write-after-read wait (before the first exchange's stores) runs a
-// gate instead: used when the exchange buffer is released by something other than this transform.
-template <class Gate>
-struct GatedCtaSync {
-  const Gate& gate;
-  mutable bool open = false;
-  __device__ __forceinline__ void operator()() const { __syncthreads(); }
-  __device__ __forceinline__ void war_arrive() const { __syncthreads(); }
-  __device__ __forceinline__ void war_wait() const {
-    if (!open) gate();
-    open = true;
-  }
-};
-#ifndef HC_TMA1_FWD
-#define HC_TMA1_FWD 1
-#endif
 // ------------------------------- column-tile pfft, tensor-map TMA, one tile buffer --
 // Blocks too long for two tile buffers at the full tile width (c4's 4096-point columns: one
 // buffer of 2 columns is 139 KB) still overlap their copies with the butterflies:
@@ -1580,35 +1634,15 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     ph ^= 1;
     double2 v[Cfg::E];
     load_pass0<SYM, Cfg>(v, a, tp, IN + g, GC, p.v, tid);
-#if HC_TMA1_FWD == 0
-    if (leader) bulk_wait_read();  // the previous tile's tensor stores have read X
-    __syncthreads();               // IN is consumed, X is free
-    if (leader) issue(t + gridDim.x);
-    fft_forward<Cfg, CtaSync, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, CtaSync(), p0);
-#else
     // one barrier behind the pass-0 butterflies says both "IN is consumed" (the next tile's copy
     // may start) and "X is free" (the previous tile's tensor stores have read it)
     auto gate = [&]() HC_INL {
-#if HC_TMA1_FWD == 1
       if (leader) bulk_wait_read();
-#endif
       __syncthreads();
       if (leader) issue(t + gridDim.x);
     };
     const GatedCtaSync<decltype(gate)> gs{gate};
     fft_forward<Cfg, GatedCtaSync<decltype(gate)>, P0Res<SYM>, NoHook, GC>(v, X + g, mt, tid, gs, p0);
-#endif
-#if HC_TMA1_FWD == 2
-    // the block leaves from registers (coalesced GC-column runs), nothing waits for X
-    const long long ob = p.lout.base(t * GC + g), oes = p.lout.es;
-    double2* F = (double2*)p.F;
-    sfor<CL>([&](auto Ci) HC_INL {
-      constexpr int c = Ci;
-      const int beta = tid + c * T;
-      if (bvalid<Cfg, Cfg::P - 1>(c, tid))
-        sfor<RL>([&](auto Ki) HC_INL { F[ob + (beta + (long long)RpL * Ki) * oes] = v[c * RL + Ki]; });
-    });
-#else
     // (fft_forward ends its last exchange with a CTA barrier: every read of X is done, X takes the block [k][GC])
     sfor<CL>([&](auto Ci) HC_INL {
       constexpr int c = Ci;
@@ -1625,7 +1659,6 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
         tma_tensor_store_3d(&mout, c0, r * tm.box_out, c2, X + (size_t)r * tm.box_out * GC);
       bulk_commit();
     }
-#endif
   }
   if (leader) bulk_wait_all();
 }
