@@ -32,9 +32,13 @@
 #include "slab.hpp"
 
 namespace hc {
-void registry_sym0(KernelEntry* out, int* count);
-void registry_sym1(KernelEntry* out, int* count);
-void registry_sym2(KernelEntry* out, int* count);
+// each symmetry's table comes from two translation units (a: blocks up to 3072 points, b: the rest)
+void registry_sym0_a(KernelEntry* out, int* count);
+void registry_sym0_b(KernelEntry* out, int* count);
+void registry_sym1_a(KernelEntry* out, int* count);
+void registry_sym1_b(KernelEntry* out, int* count);
+void registry_sym2_a(KernelEntry* out, int* count);
+void registry_sym2_b(KernelEntry* out, int* count);
 // in-place two-residue convolution kernel (conv_ip.cuh, inst_ip.cu), by complex FFT length
 const void* conv_ip_fn(int sym, int Bc);
 size_t conv_ip_smem_bytes(int Bc, int tabn);
@@ -159,9 +163,13 @@ struct Registry {
   KernelEntry e[3][32];
   int n[3] = {0, 0, 0};
   Registry() {
-    hc::registry_sym0(e[0], &n[0]);
-    hc::registry_sym1(e[1], &n[1]);
-    hc::registry_sym2(e[2], &n[2]);
+    n[0] = n[1] = n[2] = 0;
+    hc::registry_sym0_a(e[0], &n[0]);
+    hc::registry_sym0_b(e[0], &n[0]);
+    hc::registry_sym1_a(e[1], &n[1]);
+    hc::registry_sym1_b(e[1], &n[1]);
+    hc::registry_sym2_a(e[2], &n[2]);
+    hc::registry_sym2_b(e[2], &n[2]);
   }
 };
 const Registry& registry() {

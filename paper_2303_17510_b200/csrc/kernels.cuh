@@ -1308,7 +1308,9 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols_pp(FwdArgs p) 
   const P0Res<SYM> p0{&a, tp, p.v};
   const int rows = a.S;
   const int bufn = GC * (rows > Cfg::XS ? rows : Cfg::XS);
-  double2* buf[2] = {smem + a.tabn, smem + a.tabn + bufn};
+  // (buffer k & 1 is addressed by arithmetic on the shared-memory base: selecting from an array of
+  // pointers hides the address space from the compiler and every access turns generic, LD.E / ST.E)
+  double2* const buf0 = smem + a.tabn;
   const long long ntiles = (p.lin.count + GC - 1) / GC;
   const long long es = p.lin.es;
   auto gather = [&](long long t, double2* B) HC_INL {
@@ -1319,12 +1321,12 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_fwd_cols_pp(FwdArgs p) 
     }
     cp_async_commit();
   };
-  gather(blockIdx.x, buf[0]);
+  gather(blockIdx.x, buf0);
   int k = 0;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    double2* X = buf[k & 1];
+    double2* X = buf0 + (k & 1) * bufn;
     __syncthreads();  // the previous tile's exchanges in the other buffer are finished
-    gather(t + gridDim.x, buf[(k + 1) & 1]);
+    gather(t + gridDim.x, buf0 + ((k + 1) & 1) * bufn);
     cp_async_wait<1>();
     __syncthreads();  // tile t has landed (every thread's copies)
     const long long item = t * GC + g;
@@ -1360,7 +1362,9 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols_pp(BwdArgs p) 
   const P0Res<SYM> p0{&a, tp, p.v};
   constexpr int rows = Cfg::N;  // block values (complex)
   constexpr int bufn = GC * Cfg::XS;
-  double2* buf[2] = {smem + a.tabn, smem + a.tabn + bufn};
+  // (buffer k & 1 is addressed by arithmetic on the shared-memory base: selecting from an array of
+  // pointers hides the address space from the compiler and every access turns generic, LD.E / ST.E)
+  double2* const buf0 = smem + a.tabn;
   const long long ntiles = (p.lin.count + GC - 1) / GC;
   const long long ies = p.lin.es;
   const double2* F = (const double2*)p.F;
@@ -1372,12 +1376,12 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1) k_pfft_bwd_cols_pp(BwdArgs p) 
     }
     cp_async_commit();
   };
-  gather(blockIdx.x, buf[0]);
+  gather(blockIdx.x, buf0);
   int k = 0;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
-    double2* X = buf[k & 1];
+    double2* X = buf0 + (k & 1) * bufn;
     __syncthreads();
-    gather(t + gridDim.x, buf[(k + 1) & 1]);
+    gather(t + gridDim.x, buf0 + ((k + 1) & 1) * bufn);
     cp_async_wait<1>();
     __syncthreads();
     const long long item = t * GC + g;
@@ -1451,7 +1455,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   // tensor copies need 128-byte-aligned shared addresses (the dynamic segment follows the static
   // mbarriers, so align the absolute address; the host adds the slack)
   double2* buf0 = align_smem128(smem + a.tabn);
-  double2* buf[2] = {buf0, buf0 + tm.bufn};
+  // (buffer b is buf0 + b * bufn: arithmetic on the shared-memory base keeps the accesses LDS / STS)
   const long long ntiles = p.lin.count / GC;
   const bool leader = threadIdx.x == 0;
   const int kBox = tm.box_in;
@@ -1462,7 +1466,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     const long long item = t * GC;
     const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
     mbar_expect_tx(&bars[b], box_bytes * (uint32_t)nbox_in);
-    for (int r = 0; r < nbox_in; ++r) tma_tensor_load_3d(buf[b] + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
+    for (int r = 0; r < nbox_in; ++r) tma_tensor_load_3d(buf0 + (size_t)b * tm.bufn + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
   };
   if (leader) {
     tma_prefetch_map(&min);
@@ -1477,7 +1481,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   int k = 0;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int b = k & 1;
-    double2* X = buf[b];
+    double2* X = buf0 + (size_t)b * tm.bufn;
     mbar_wait(&bars[b], ph[b]);
     ph[b] ^= 1;
     double2 v[Cfg::E];
@@ -1531,7 +1535,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   const double2* tp = a.tabn >= a.tabfull ? tb : a.tab;
   const P0Res<SYM> p0{&a, tp, p.v};
   double2* buf0 = align_smem128(smem + a.tabn);
-  double2* buf[2] = {buf0, buf0 + tm.bufn};
+  // (buffer b is buf0 + b * bufn: arithmetic on the shared-memory base keeps the accesses LDS / STS)
   const long long ntiles = p.lin.count / GC;
   const bool leader = threadIdx.x == 0;
   const int kBox = tm.box_in;
@@ -1542,7 +1546,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
     const long long item = t * GC;
     const int c0 = (int)(2 * (item % tm.inner)), c2 = (int)(item / tm.inner);
     mbar_expect_tx(&bars[b], box_bytes * (uint32_t)nbox);
-    for (int r = 0; r < nbox; ++r) tma_tensor_load_3d(buf[b] + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
+    for (int r = 0; r < nbox; ++r) tma_tensor_load_3d(buf0 + (size_t)b * tm.bufn + (size_t)r * kBox * GC, &min, c0, r * kBox, c2, &bars[b]);
   };
   if (leader) {
     tma_prefetch_map(&min);
@@ -1556,7 +1560,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
   int k = 0;
   for (long long t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
     const int b = k & 1;
-    double2* X = buf[b];
+    double2* X = buf0 + (size_t)b * tm.bufn;
     // the other buffer's exchanges (previous tile) ended at the barrier closing that tile
     if (leader) issue(t + gridDim.x, b ^ 1);
     mbar_wait(&bars[b], ph[b]);
@@ -1716,7 +1720,7 @@ __global__ void __launch_bounds__(Cfg::T * GC, 1)
       if (bvalid<Cfg, Cfg::P - 1>(c, tid))
         sfor<RL>([&](auto Ki) HC_INL {
           const int row = beta + RpL * Ki;
-          v[c * RL + Ki] = (row < rows_s ? S : X)[row * GC + g];
+          v[c * RL + Ki] = X[(row < rows_s ? tm.bufn : 0) + row * GC + g];  // S = X + bufn (one shared base)
         });
     });
     __syncthreads();  // the block is in registers: S may be refilled, the exchanges may use X

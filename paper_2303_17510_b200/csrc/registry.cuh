@@ -202,48 +202,55 @@ KernelEntry make_naive_entry() {
 #ifndef HC_R1024_MINB
 #define HC_R1024_MINB 1
 #endif
-// Radix plans (complex FFT length -> passes, threads per line group, groups per CTA).
-template <int SYM>
+// Radix plans (complex FFT length -> passes, threads per line group, groups per CTA).  The table of a
+// symmetry is built by two translation units (PART 0: blocks up to 3072 points, PART 1: the long
+// blocks and the direct-sum entry) so that the build's critical path is half a symmetry.
+template <int SYM, int PART>
 inline void build_registry(KernelEntry* out, int* count) {
-  int k = 0;
+  int k = *count;
 #ifdef HC_REGISTRY_MIN
   // development builds (make VARIANT=dev EXTRA=-DHC_REGISTRY_MIN): the plans of c3 / c4 / c5 only
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
+  if constexpr (PART == 0) {
+    out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
+  } else {
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
 #ifdef HC_REGISTRY_C2  // + c2's 6144-point plan (the in-place kernel's host plumbing hangs off it)
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
 #endif
-  out[k++] = make_naive_entry<SYM>();
-  *count = k;
+    out[k++] = make_naive_entry<SYM>();
+  }
 #else
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4, false, 4>("8x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4, false, 4>("16x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
-  // 384 = 8x8x6: the explicit 768-point Hermitian block of c5's z axis (M = 766)
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 6>, 64>, 1, false, 8>("8x8x6");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, HC_R1024_G, false, HC_R1024_MINB>("16x16x4");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1, true, 3>("16x16x8");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
-  // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
+  if constexpr (PART == 0) {
+    out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8>, 32>, 4, false, 4>("8x8");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 8>, 32>, 4, false, 4>("16x8");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<4, 8, 8>, 32>, 4, false, 4>("4x8x8");
+    // 384 = 8x8x6: the explicit 768-point Hermitian block of c5's z axis (M = 766)
+    out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 6>, 64>, 1, false, 8>("8x8x6");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<8, 8, 8>, 64>, HC_R512_G, false, HC_R512_MINB>("8x8x8");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 3>, 64>, 2>("16x16x3");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 4>, 64>, HC_R1024_G, false, HC_R1024_MINB>("16x16x4");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 6>, 96>, 1>("16x16x6");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 8>, 128>, 1, true, 3>("16x16x8");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 12>, 192>, 1>("16x16x12");
+  } else {
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 16>, 256>, 1, HC_R4096_SMEM_STASH, HC_R4096_MINB>("16x16x16");
+    // measured on B200 (r01): 16x16x24/T384 1.146 ms for c2, 8x8x8x12/T768 1.231 ms
 #if HC_R6144_PLAN == 2
-  out[k++] = make_entry<SYM, FFTCfg<Radices<24, 16, 16>, 256>, 1>("24x16x16");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<24, 16, 16>, 256>, 1>("24x16x16");
 #else
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 16, 24>, 384>, 1>("16x16x24");
 #endif
-  // radix-7 plan: 3584 = 16 x 14 x 16 (the 7-smooth sizes of SPEC.md:523; DFT14 = 2 x 7 with the
-  // pair-form DFT7): blocks of 3584 complex / 7168 Hermitian points
-  out[k++] = make_entry<SYM, FFTCfg<Radices<16, 14, 16>, 256>, 1>("16x14x16");
-  // radix-5 plan: 6000 = 10 x 24 x 25 (the 5-smooth sizes of SPEC.md:523's search space, e.g.
-  // c2's m = 6000 = L, p = 1, q = 2)
-  out[k++] = make_entry<SYM, FFTCfg<Radices<10, 24, 25>, 320>, 1>("10x24x25");
-  out[k++] = make_naive_entry<SYM>();
+    // radix-7 plan: 3584 = 16 x 14 x 16 (the 7-smooth sizes of SPEC.md:523; DFT14 = 2 x 7 with the
+    // pair-form DFT7): blocks of 3584 complex / 7168 Hermitian points
+    out[k++] = make_entry<SYM, FFTCfg<Radices<16, 14, 16>, 256>, 1>("16x14x16");
+    // radix-5 plan: 6000 = 10 x 24 x 25 (the 5-smooth sizes of SPEC.md:523's search space, e.g.
+    // c2's m = 6000 = L, p = 1, q = 2)
+    out[k++] = make_entry<SYM, FFTCfg<Radices<10, 24, 25>, 320>, 1>("10x24x25");
+    out[k++] = make_naive_entry<SYM>();
+  }
+#endif
   *count = k;
-#endif
 }
 
 }  // namespace hc

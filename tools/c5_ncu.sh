@@ -10,6 +10,6 @@ cap() {  # name kernel-regex skip
   ncu -i /tmp/$1.ncu-rep --page raw --csv > gpurun_out/$1_raw.csv 2>/dev/null
 }
 cap c5_fwdcols_y k_pfft_fwd_cols 10
-cap c5_conv k_conv1d_pp 10
+cap c5_conv k_conv1d_pp 2
 cap c5_fwdcols_x k_pfft_fwd_cols 1
-cap c5_bwdcols_y k_pfft_bwd_cols 10
+cap c5_bwdcols_y k_pfft_bwd_cols 5
