@@ -1497,13 +1497,15 @@ void* CudaSlabOps::alloc(size_t elems) {
 void CudaSlabOps::fwd(size_t r, const void* f, void* F) {
   const hslab::Geometry& g = st->g;
   const long long nxz = (long long)(g.nx() * g.Z), Z = (long long)g.Z;
-  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, nxz, 0, 1, nxz};
+  // (the spectrum's lines described with the same inner extent as the slab's, Z columns per x row:
+  // the tensor-map column tiles need matching tile coordinates on both sides)
+  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, Z, Z, 1, nxz};
   launch_fwd(st->ay, lin, lspec, (const double2*)f, F, (int)r, 0, s);
 }
 void CudaSlabOps::bwd(size_t r, const void* W, void* h, bool acc, double scale) {
   const hslab::Geometry& g = st->g;
   const long long nxz = (long long)(g.nx() * g.Z), Z = (long long)g.Z;
-  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, nxz, 0, 1, nxz};
+  const hc::Lines lin{nxz, Z, (long long)g.Ly * Z, 1, Z}, lspec{nxz, Z, Z, 1, nxz};
   launch_bwd(st->ay, lspec, lin, W, (double2*)h, acc ? (const double2*)h : nullptr, scale, (int)r, 0, s);
 }
 void CudaSlabOps::inner(size_t count, void* const* T) {
